@@ -1,0 +1,271 @@
+// harness.cu — the batched measurement harness:
+// dispatch (sketch, point) -> launcher, candidate execution, verification and
+// timing.  Candidates "are executed and timed"; each trial is "the
+// observation of the execution of an actual schedule".
+//
+// One rank's share of a batch goes through two pipelined phases on the
+// tuner's stream, with ONE host synchronisation per phase (not per candidate):
+//   1. verify: poison y (NaN), launch the candidate between two events, reduce
+//      max_err into a device slot (verify_maxerr); D2H all slots; sync.
+//   2. time:   for every candidate that verified, W untimed launches, then R
+//      repeats of a CUDA graph of `number` back-to-back launches, each repeat
+//      bracketed by events (number = 20 us / t_verify, clamped to [1, 100]);
+//      sync; cost = median over repeats of elapsed / number (R-M2).
+// Graph capture and instantiation of candidate j+1 on the host overlap the
+// GPU executing candidate j.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "internal.hpp"
+#include "kernels/common.cuh"
+
+namespace db200 {
+
+cudaError_t launch_reference(const ShapeInfo& s, const void* x, const void* w, float* yref, float* aref,
+                             cudaStream_t st);
+cudaError_t launch_verify(const float* y, const float* r, const float* a, long long n, unsigned int* out,
+                          int num_sms, cudaStream_t st);
+void set_capturing(bool on);
+
+static tuner_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(TUNER_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CU(call)                                            \
+    do {                                                    \
+        cudaError_t e_ = (call);                            \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+// launcher + runtime knobs of a point
+static LaunchFn resolve(const Tuner* t, const Pt& p, int& split) {
+    int32_t v[TUNER_MAX_KNOBS];
+    t->values_of(p, v);
+    const int32_t sk = t->spaces[p.pos].sketch;
+    switch (sk) {
+        case SK_SIMT_GEMM_F32:
+        case SK_SIMT_IGEMM_CONV_F32:
+            split = v[5];
+            return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[4]));
+        case SK_TC_GEMM_BF16:
+        case SK_TC_IGEMM_CONV_BF16:
+            split = v[4];
+            return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], 0));
+        default: return nullptr;
+    }
+}
+
+// process-wide pool of timing events (per device), grown on demand
+static std::vector<cudaEvent_t>& event_pool(int dev) {
+    static std::vector<std::vector<cudaEvent_t>> pools(64);
+    return pools[dev & 63];
+}
+static tuner_status ensure_events(int dev, size_t n) {
+    auto& pool = event_pool(dev);
+    while (pool.size() < n) {
+        cudaEvent_t e;
+        CU(cudaEventCreate(&e));
+        pool.push_back(e);
+    }
+    return TUNER_OK;
+}
+
+namespace {
+struct GpuMeasurer : Measurer {
+    Tuner* t;
+    int dev = 0, nsm = 148;
+    cudaStream_t st = nullptr, cap = nullptr;
+    float* ref = nullptr;
+    float* absref = nullptr;
+    bool own_ref = false;
+    unsigned* d_err = nullptr;
+    unsigned* h_err = nullptr;
+    size_t err_cap = 0;
+    double tol;
+
+    ~GpuMeasurer() override {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(dev);
+        if (own_ref) {
+            cudaFree(ref);
+            cudaFree(absref);
+        }
+        if (d_err) cudaFree(d_err);
+        if (h_err) cudaFreeHost(h_err);
+        if (cap) cudaStreamDestroy(cap);
+        cudaSetDevice(cur);
+    }
+
+    tuner_status init() {
+        CU(cudaGetDevice(&dev));
+        CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        st = (cudaStream_t)t->opts.stream;
+        CU(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        tol = t->info.dtype == TUNER_F32 ? 1e-4 : 2e-2;  // north_star tolerances
+        if (t->opts.y_ref && t->opts.y_absref) {
+            ref = const_cast<float*>(t->opts.y_ref);
+            absref = const_cast<float*>(t->opts.y_absref);
+        } else if (t->opts.verify) {
+            own_ref = true;
+            CU(cudaMalloc(&ref, (size_t)t->info.y_elems * sizeof(float)));
+            CU(cudaMalloc(&absref, (size_t)t->info.y_elems * sizeof(float)));
+            CU(launch_reference(t->info, t->opts.x, t->opts.w, ref, absref, st));
+            CU(cudaStreamSynchronize(st));
+        }
+        return TUNER_OK;
+    }
+
+    bool valid(const Pt& p) override {
+        int32_t v[TUNER_MAX_KNOBS];
+        t->values_of(p, v);
+        if (!sketch_valid(t->spaces[p.pos].sketch, t->info, v)) return false;
+        int split = 1;
+        return resolve(t, p, split) != nullptr;
+    }
+
+    tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out) override {
+        const size_t n = pts.size();
+        out.assign(n, Result{});
+        if (n == 0) return TUNER_OK;
+        CU(cudaSetDevice(dev));
+        const int R = t->opts.repeats, W = t->opts.warmup;
+        tuner_status s = ensure_events(dev, n * (size_t)(R + 3));
+        if (s != TUNER_OK) return s;
+        auto& ev = event_pool(dev);
+        if (err_cap < n) {
+            if (d_err) cudaFree(d_err);
+            if (h_err) cudaFreeHost(h_err);
+            CU(cudaMalloc(&d_err, n * sizeof(unsigned)));
+            CU(cudaMallocHost(&h_err, n * sizeof(unsigned)));
+            err_cap = n;
+        }
+        std::vector<LaunchFn> fn(n);
+        std::vector<int> split(n, 1);
+        std::vector<char> launched(n, 0);
+        for (size_t j = 0; j < n; ++j) fn[j] = resolve(t, pts[j], split[j]);
+        const size_t ybytes = (size_t)t->info.y_elems * sizeof(float);
+        LaunchCtx ctx{&t->info, t->opts.x, t->opts.w, t->opts.y, 1, st, nsm};
+
+        // ---- phase 1: verification run (also the first, untimed-for-cost launch)
+        CU(cudaMemsetAsync(d_err, 0, n * sizeof(unsigned), st));
+        for (size_t j = 0; j < n; ++j) {
+            ctx.split = split[j];
+            if (t->opts.verify) CU(cudaMemsetAsync(t->opts.y, 0xFF, ybytes, st));
+            CU(cudaEventRecord(ev[2 * j], st));
+            cudaError_t e = fn[j] ? fn[j](ctx) : cudaErrorInvalidDeviceFunction;
+            CU(cudaEventRecord(ev[2 * j + 1], st));
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                out[j].status = TUNER_S_LAUNCH_FAIL;
+                continue;
+            }
+            launched[j] = 1;
+            if (t->opts.verify)
+                CU(launch_verify((const float*)t->opts.y, ref, absref, t->info.y_elems, d_err + j, nsm, st));
+        }
+        CU(cudaMemcpyAsync(h_err, d_err, n * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        std::vector<double> tver(n, 0.0);
+        for (size_t j = 0; j < n; ++j) {
+            if (!launched[j]) continue;
+            float ms = 0.f;
+            CU(cudaEventElapsedTime(&ms, ev[2 * j], ev[2 * j + 1]));
+            tver[j] = ms * 1e6;  // ns
+            float err;
+            std::memcpy(&err, &h_err[j], sizeof(float));
+            out[j].max_err = t->opts.verify ? (double)err : 0.0;
+            if (t->opts.verify && !(err <= tol)) out[j].status = TUNER_S_WRONG;
+            else if (ms > t->opts.timeout_ms) out[j].status = TUNER_S_TIMEOUT;
+        }
+
+        // ---- phase 2: timing
+        std::vector<cudaGraphExec_t> execs(n, nullptr);
+        std::vector<int> number(n, 1);
+        const size_t tb = 2 * n;  // timing events start here
+        for (size_t j = 0; j < n; ++j) {
+            if (out[j].status != TUNER_S_OK) continue;
+            ctx.split = split[j];
+            int num = t->opts.number;
+            if (num <= 0) {
+                double want = 20000.0 / std::max(tver[j], 1.0);
+                num = (int)std::min(100.0, std::max(1.0, std::ceil(want)));
+            }
+            number[j] = num;
+            for (int i = 0; i < W; ++i) {
+                cudaError_t e = fn[j](ctx);
+                if (e != cudaSuccess) return cuda_fail(e, "warm-up launch");
+            }
+            LaunchCtx cc = ctx;
+            cc.stream = cap;
+            set_capturing(true);
+            cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+            for (int i = 0; i < num && e == cudaSuccess; ++i) e = fn[j](cc);
+            cudaGraph_t g = nullptr;
+            cudaError_t e2 = cudaStreamEndCapture(cap, &g);
+            set_capturing(false);
+            if (e != cudaSuccess) return cuda_fail(e, "graph capture");
+            if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamEndCapture");
+            e = cudaGraphInstantiate(&execs[j], g, 0);
+            cudaGraphDestroy(g);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+            const size_t b = tb + j * (size_t)(R + 1);
+            CU(cudaEventRecord(ev[b], st));
+            for (int r = 0; r < R; ++r) {
+                CU(cudaGraphLaunch(execs[j], st));
+                count_launches(num);
+                CU(cudaEventRecord(ev[b + r + 1], st));
+            }
+        }
+        cudaError_t se = cudaStreamSynchronize(st);
+        for (auto ge : execs)
+            if (ge) cudaGraphExecDestroy(ge);
+        if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize (timing)");
+        std::vector<double> per(R);
+        for (size_t j = 0; j < n; ++j) {
+            if (out[j].status != TUNER_S_OK) {
+                out[j].cost_ns = INFINITY;
+                continue;
+            }
+            const size_t b = tb + j * (size_t)(R + 1);
+            for (int r = 0; r < R; ++r) {
+                float ms = 0.f;
+                CU(cudaEventElapsedTime(&ms, ev[b + r], ev[b + r + 1]));
+                per[r] = (double)ms * 1e6 / number[j];
+            }
+            std::sort(per.begin(), per.end());
+            out[j].cost_ns = (R % 2) ? per[R / 2] : 0.5 * (per[R / 2 - 1] + per[R / 2]);
+        }
+        return TUNER_OK;
+    }
+};
+}  // namespace
+
+tuner_status make_gpu_measurer(Tuner* t, std::unique_ptr<Measurer>& out) {
+    std::unique_ptr<GpuMeasurer> m(new GpuMeasurer());
+    m->t = t;
+    tuner_status s = m->init();
+    if (s != TUNER_OK) return s;
+    out = std::move(m);
+    return TUNER_OK;
+}
+
+tuner_status gpu_kernel_run(const Tuner* t, const Pt& p, const tuner_buffers* buf, void* stream) {
+    int split = 1;
+    LaunchFn fn = resolve(t, p, split);
+    if (!fn) return fail(TUNER_ERANGE, "schedule not compiled");
+    int nsm = 148, dev = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    LaunchCtx ctx{&t->info, buf->x, buf->w, buf->y, split, (cudaStream_t)stream, nsm};
+    CU(fn(ctx));
+    return TUNER_OK;
+}
+
+tuner_status gpu_reference(const Tuner* t, const tuner_buffers* buf, float* y_ref, float* y_absref, void* stream) {
+    CU(launch_reference(t->info, buf->x, buf->w, y_ref, y_absref, (cudaStream_t)stream));
+    return TUNER_OK;
+}
+
+}  // namespace db200

@@ -1,0 +1,33 @@
+// common.cuh — launch context and registry shared by the kernel family.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../shape.hpp"
+
+namespace db200 {
+
+// Everything a candidate launch needs; built by the harness per launch.
+struct LaunchCtx {
+    const ShapeInfo* sh;
+    const void* x;
+    const void* w;
+    void* y;
+    int split;             // runtime SPLIT_K knob
+    cudaStream_t stream;
+    int num_sms;
+};
+
+typedef cudaError_t (*LaunchFn)(const LaunchCtx&);
+
+// Registry of compiled instantiations: key = (sketch, compile-time knob values).
+uint64_t kernel_key(int32_t sketch, int a, int b, int c, int d, int e);
+void registry_add(uint64_t key, LaunchFn fn);
+LaunchFn registry_find(uint64_t key);
+
+// Counter of candidate-kernel launches (graph nodes included).
+void count_launches(int64_t n);
+void set_capturing(bool on);
+
+}  // namespace db200

@@ -1,0 +1,148 @@
+// refverify.cu — the library's own verification reference and the per-candidate
+// verification kernel.
+//
+// naive_ref_*: the naive schedule of Def. 2.1 ("replaces each linear
+// index ... with a loop"), one thread per output, fp64 accumulation; it also
+// produces A = sum |x||w| (the forward-error denominator, R-V1).  Run once per
+// tuner; the product never calls the test oracle.
+//
+// verify_maxerr: err = max_i |y_i - r_i| / max(a_i, 1e-30) over all outputs
+// (R-V1), NaN/inf -> +inf.  HBM-bound: reads 12 B per output element
+// (y, r, a as fp32) with 128-bit loads, grid-stride, warp-shuffle max, one
+// atomicMax per block on the float's bit pattern (non-negative floats order
+// like their bits).
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace db200 {
+
+template <typename T>
+__device__ __forceinline__ double as_f64(T v);
+template <>
+__device__ __forceinline__ double as_f64<float>(float v) { return (double)v; }
+template <>
+__device__ __forceinline__ double as_f64<__nv_bfloat16>(__nv_bfloat16 v) { return (double)__bfloat162float(v); }
+
+template <typename T>
+__global__ void naive_ref_gemm(const T* __restrict__ X, const T* __restrict__ W, float* __restrict__ Y,
+                               float* __restrict__ Aabs, long long batch, long long M, long long N, long long K) {
+    long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (o >= batch * M * N) return;
+    long long b = o / (M * N), m = (o / N) % M, n = o % N;
+    const T* x = X + (b * M + m) * K;
+    const T* w = W + (b * N + n) * K;
+    double acc = 0.0, aab = 0.0;
+    for (long long k = 0; k < K; ++k) {
+        double xv = as_f64(x[k]), wv = as_f64(w[k]);
+        acc += xv * wv;
+        aab += fabs(xv) * fabs(wv);
+    }
+    Y[o] = (float)acc;
+    Aabs[o] = (float)aab;
+}
+
+template <typename T>
+__global__ void naive_ref_conv(const T* __restrict__ X, const T* __restrict__ W, float* __restrict__ Y,
+                               float* __restrict__ Aabs, int N, int H, int Wd, int C, int K, int R, int S, int P,
+                               int Q, int sh, int sw, int ph, int pw, int dh, int dw) {
+    long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    long long total = (long long)N * P * Q * K;
+    if (o >= total) return;
+    int k = (int)(o % K);
+    int q = (int)((o / K) % Q);
+    int p = (int)((o / ((long long)K * Q)) % P);
+    int n = (int)(o / ((long long)K * Q * P));
+    double acc = 0.0, aab = 0.0;
+    for (int r = 0; r < R; ++r) {
+        int h = p * sh - ph + r * dh;
+        if (h < 0 || h >= H) continue;
+        for (int s = 0; s < S; ++s) {
+            int w = q * sw - pw + s * dw;
+            if (w < 0 || w >= Wd) continue;
+            const T* xp = X + (((long long)n * H + h) * Wd + w) * C;
+            const T* wp = W + (((long long)k * R + r) * S + s) * C;
+            for (int c = 0; c < C; ++c) {
+                double xv = as_f64(xp[c]), wv = as_f64(wp[c]);
+                acc += xv * wv;
+                aab += fabs(xv) * fabs(wv);
+            }
+        }
+    }
+    Y[o] = (float)acc;
+    Aabs[o] = (float)aab;
+}
+
+__device__ __forceinline__ float err_of(float y, float r, float a) {
+    float d = fabsf(y - r) / fmaxf(a, 1e-30f);
+    return (isfinite(y) && !isnan(d)) ? d : INFINITY;
+}
+
+__global__ void verify_maxerr(const float* __restrict__ y, const float* __restrict__ r, const float* __restrict__ a,
+                              long long n, unsigned int* __restrict__ out) {
+    float m = 0.f;
+    const long long n4 = n / 4;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const float4* y4 = reinterpret_cast<const float4*>(y);
+    const float4* r4 = reinterpret_cast<const float4*>(r);
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 yv = __ldcs(y4 + i), rv = __ldg(r4 + i), av = __ldg(a4 + i);
+        m = fmaxf(m, err_of(yv.x, rv.x, av.x));
+        m = fmaxf(m, err_of(yv.y, rv.y, av.y));
+        m = fmaxf(m, err_of(yv.z, rv.z, av.z));
+        m = fmaxf(m, err_of(yv.w, rv.w, av.w));
+    }
+    for (long long i = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
+        m = fmaxf(m, err_of(y[i], r[i], a[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ float wmax[32];
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? wmax[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (threadIdx.x == 0) atomicMax(out, __float_as_uint(m));
+    }
+}
+
+cudaError_t launch_reference(const ShapeInfo& s, const void* x, const void* w, float* yref, float* aref,
+                             cudaStream_t st) {
+    const long long total = s.y_elems;
+    const int bs = 128;
+    const unsigned grid = (unsigned)((total + bs - 1) / bs);
+    if (s.op == TUNER_OP_CONV2D) {
+        if (s.dtype == TUNER_F32)
+            naive_ref_conv<float><<<grid, bs, 0, st>>>((const float*)x, (const float*)w, yref, aref, (int)s.n, (int)s.h,
+                                                       (int)s.w, (int)s.c, (int)s.k, (int)s.r, (int)s.s, (int)s.p,
+                                                       (int)s.q, s.sh, s.sw, s.ph, s.pw, s.dh, s.dw);
+        else
+            naive_ref_conv<__nv_bfloat16><<<grid, bs, 0, st>>>(
+                (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, yref, aref, (int)s.n, (int)s.h, (int)s.w, (int)s.c,
+                (int)s.k, (int)s.r, (int)s.s, (int)s.p, (int)s.q, s.sh, s.sw, s.ph, s.pw, s.dh, s.dw);
+    } else {
+        if (s.dtype == TUNER_F32)
+            naive_ref_gemm<float><<<grid, bs, 0, st>>>((const float*)x, (const float*)w, yref, aref, s.batch, s.M, s.N,
+                                                       s.K);
+        else
+            naive_ref_gemm<__nv_bfloat16><<<grid, bs, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)w, yref,
+                                                               aref, s.batch, s.M, s.N, s.K);
+    }
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_verify(const float* y, const float* r, const float* a, long long n, unsigned int* out,
+                          int num_sms, cudaStream_t st) {
+    const int bs = 512;
+    long long want = (n / 4 + bs - 1) / bs;
+    long long cap = (long long)num_sms * 4;
+    unsigned grid = (unsigned)(want < 1 ? 1 : (want > cap ? cap : want));
+    verify_maxerr<<<grid, bs, 0, st>>>(y, r, a, n, out);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace db200

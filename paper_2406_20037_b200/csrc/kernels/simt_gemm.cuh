@@ -1,0 +1,363 @@
+// simt_gemm.cuh — sketches SIMT_GEMM_F32 and SIMT_IGEMM_CONV_F32.
+//
+// One fixed sequence of transformations (a "sketch", Def. 2.1) of
+// the naive loop nest Y[m,n] = sum_k A[m,k] B[n,k]: split m and n into BM x BN
+// block tiles bound to CTAs, split each block tile into TT x TT register tiles
+// bound to threads, split k into BK-wide steps staged through shared memory
+// (double-buffered through registers so the next tile's global loads overlap
+// this tile's FMAs), unroll the inner k loop by UNROLL, and optionally split
+// the k range across SPLIT_K CTAs whose partial sums are reduced with vector
+// atomics.  The annotations (BM, BN, BK, TT, UNROLL, SPLIT_K) are the knobs.
+//
+// CONV = true is the implicit-GEMM view of conv2d (NHWC x KRSC -> NPQK):
+// A[m, kk] = X[n, p*sh-ph+r*dh, q*sw-pw+s*dw, c] with m = (n,p,q), kk = (r,s,c),
+// gathered on the fly (zero outside the image); B = W viewed as [K][R*S*C].
+//
+// FP32 on the CUDA cores (north_star: "The fp32 SIMT variants stay on CUDA
+// cores"); 128-bit global loads whenever the reduction run allows (VEC4).
+#pragma once
+#include "common.cuh"
+
+namespace db200 {
+
+struct SimtParams {
+    const float* __restrict__ A;
+    const float* __restrict__ B;
+    float* __restrict__ C;
+    int M, N, K;
+    long long sA, sB, sC;  // batch strides
+    int ktiles, kt_per_split, split;
+    // implicit GEMM (conv) geometry
+    int H, W, Cin, P, Q, S, sh, sw, ph, pw, dh, dw;
+    int vec4;
+};
+
+template <int BM, int BN, int BK, int TT>
+struct SimtCfg {
+    static constexpr int NT = (BM / TT) * (BN / TT);
+    static constexpr int TX = BN / TT;
+    static constexpr int LDA = BM + 4;
+    static constexpr int LDB = BN + 4;
+    static constexpr int SA1 = (BM * BK + NT - 1) / NT;      // scalar staging per thread
+    static constexpr int SB1 = (BN * BK + NT - 1) / NT;
+    static constexpr int SA4 = (BM * BK / 4 + NT - 1) / NT;  // float4 staging per thread
+    static constexpr int SB4 = (BN * BK / 4 + NT - 1) / NT;
+    static constexpr int STAGE_FLOATS = (SA1 > 4 * SA4 ? SA1 : 4 * SA4) + (SB1 > 4 * SB4 ? SB1 : 4 * SB4);
+    static constexpr size_t SMEM = (size_t)2 * BK * (LDA + LDB) * sizeof(float) + 3 * BM * sizeof(int);
+};
+
+// compile-time half of the static validity rule (the runtime half is in sketches.cpp)
+constexpr int cdiv_c(int a, int b) { return (a + b - 1) / b; }
+constexpr int simt_stage(int BMN, int BK, int NT) {
+    return cdiv_c(BMN * BK, NT) > 4 * cdiv_c(BMN * BK / 4, NT) ? cdiv_c(BMN * BK, NT) : 4 * cdiv_c(BMN * BK / 4, NT);
+}
+constexpr bool simt_static_ok(int BM, int BN, int BK, int TT) {
+    return TT <= BM && TT <= BN && (BM / TT) * (BN / TT) <= 1024 &&
+           simt_stage(BM, BK, (BM / TT) * (BN / TT)) + simt_stage(BN, BK, (BM / TT) * (BN / TT)) <= 64;
+}
+
+// Row r of a thread's TT-row register tile -> row inside the block tile.
+// TT <= 4: contiguous; TT = 8: two 4-row groups BM/2 apart (conflict-free LDS.128).
+template <int BMN, int TT>
+__device__ __forceinline__ int tile_row(int t, int i) {
+    if constexpr (TT <= 4) return t * TT + i;
+    else return (i < 4) ? (t * 4 + i) : (BMN / 2 + t * 4 + (i - 4));
+}
+
+// (r, s, c) of reduction index kk for the implicit GEMM, by carrying from a base.
+struct RSC {
+    int r, s, c;
+};
+__device__ __forceinline__ RSC rsc_advance(RSC b, int add, int Cin, int S) {
+    b.c += add;
+    while (b.c >= Cin) {
+        b.c -= Cin;
+        if (++b.s == S) { b.s = 0; ++b.r; }
+    }
+    return b;
+}
+
+template <int BM, int BN, int BK, int TT, int UNROLL, bool CONV>
+__global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
+    simt_gemm_f32_kernel(const SimtParams p) {
+    using Cfg = SimtCfg<BM, BN, BK, TT>;
+    constexpr int NT = Cfg::NT, TX = Cfg::TX, LDA = Cfg::LDA, LDB = Cfg::LDB;
+    extern __shared__ __align__(16) float smem[];
+    float* As = smem;                              // [2][BK][LDA]
+    float* Bs = smem + 2 * BK * LDA;               // [2][BK][LDB]
+    int* rowinfo = (int*)(Bs + 2 * BK * LDB);      // CONV: [3][BM] image base, h0, w0
+
+    const int tid = threadIdx.x;
+    const int tx = tid % TX, ty = tid / TX;
+    const int m0 = blockIdx.x * BM;
+    const int n0 = blockIdx.y * BN;
+    const int bz = blockIdx.z / p.split;
+    const int kz = blockIdx.z % p.split;
+    const int kt_begin = kz * p.kt_per_split;
+    const int kt_end = min(p.ktiles, kt_begin + p.kt_per_split);
+    if (kt_begin >= kt_end) return;
+
+    const float* __restrict__ A = p.A + (CONV ? 0 : bz * p.sA);
+    const float* __restrict__ B = p.B + bz * p.sB;
+    float* __restrict__ C = p.C + bz * p.sC;
+
+    if constexpr (CONV) {
+        for (int i = tid; i < BM; i += NT) {
+            int m = m0 + i;
+            int base = 0, h0 = -(1 << 29), w0 = 0;
+            if (m < p.M) {
+                int q = m % p.Q;
+                int t = m / p.Q;
+                int pp = t % p.P;
+                int n = t / p.P;
+                base = n * p.H * p.W * p.Cin;
+                h0 = pp * p.sh - p.ph;
+                w0 = q * p.sw - p.pw;
+            }
+            rowinfo[i] = base;
+            rowinfo[BM + i] = h0;
+            rowinfo[2 * BM + i] = w0;
+        }
+        __syncthreads();
+    }
+
+    float acc[TT][TT];
+#pragma unroll
+    for (int i = 0; i < TT; ++i)
+#pragma unroll
+        for (int j = 0; j < TT; ++j) acc[i][j] = 0.f;
+
+    // staging registers: large enough for either load path
+    constexpr int SA = Cfg::SA1 > 4 * Cfg::SA4 ? Cfg::SA1 : 4 * Cfg::SA4;
+    constexpr int SB = Cfg::SB1 > 4 * Cfg::SB4 ? Cfg::SB1 : 4 * Cfg::SB4;
+    float ra[SA], rb[SB];
+
+    // A element loader (dense or implicit GEMM)
+    auto load_a1 = [&](int row, int kk, RSC rsc) -> float {
+        const int m = m0 + row;
+        if (m >= p.M || kk >= p.K) return 0.f;
+        if constexpr (CONV) {
+            const int h = rowinfo[BM + row] + rsc.r * p.dh;
+            const int w = rowinfo[2 * BM + row] + rsc.s * p.dw;
+            if ((unsigned)h >= (unsigned)p.H || (unsigned)w >= (unsigned)p.W) return 0.f;
+            return __ldg(A + rowinfo[row] + (h * p.W + w) * p.Cin + rsc.c);
+        } else {
+            return __ldg(A + (long long)m * p.K + kk);
+        }
+    };
+    auto load_a4 = [&](int row, int kk, RSC rsc) -> float4 {
+        const int m = m0 + row;
+        if (m >= p.M || kk >= p.K) return make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (CONV) {
+            const int h = rowinfo[BM + row] + rsc.r * p.dh;
+            const int w = rowinfo[2 * BM + row] + rsc.s * p.dw;
+            if ((unsigned)h >= (unsigned)p.H || (unsigned)w >= (unsigned)p.W) return make_float4(0.f, 0.f, 0.f, 0.f);
+            return __ldg(reinterpret_cast<const float4*>(A + rowinfo[row] + (h * p.W + w) * p.Cin + rsc.c));
+        } else {
+            return __ldg(reinterpret_cast<const float4*>(A + (long long)m * p.K + kk));
+        }
+    };
+
+    auto gload = [&](int kt) {
+        const int k0 = kt * BK;
+        RSC base{0, 0, 0};
+        if constexpr (CONV) {
+            int rs = k0 / p.Cin;
+            base.c = k0 - rs * p.Cin;
+            base.s = rs % p.S;
+            base.r = rs / p.S;
+        }
+        if (p.vec4) {
+            constexpr int KV = BK / 4;
+#pragma unroll
+            for (int i = 0; i < Cfg::SA4; ++i) {
+                const int e = tid + i * NT;
+                const int row = e / KV, kl = (e % KV) * 4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (e < BM * KV) {
+                    RSC rsc = base;
+                    if constexpr (CONV) rsc = rsc_advance(base, kl, p.Cin, p.S);
+                    v = load_a4(row, k0 + kl, rsc);
+                }
+                ra[4 * i + 0] = v.x; ra[4 * i + 1] = v.y; ra[4 * i + 2] = v.z; ra[4 * i + 3] = v.w;
+            }
+#pragma unroll
+            for (int i = 0; i < Cfg::SB4; ++i) {
+                const int e = tid + i * NT;
+                const int row = e / KV, kl = (e % KV) * 4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (e < BN * KV && n0 + row < p.N && k0 + kl < p.K)
+                    v = __ldg(reinterpret_cast<const float4*>(B + (long long)(n0 + row) * p.K + k0 + kl));
+                rb[4 * i + 0] = v.x; rb[4 * i + 1] = v.y; rb[4 * i + 2] = v.z; rb[4 * i + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < Cfg::SA1; ++i) {
+                const int e = tid + i * NT;
+                const int row = e / BK, kl = e % BK;
+                float v = 0.f;
+                if (e < BM * BK) {
+                    RSC rsc = base;
+                    if constexpr (CONV) rsc = rsc_advance(base, kl, p.Cin, p.S);
+                    v = load_a1(row, k0 + kl, rsc);
+                }
+                ra[i] = v;
+            }
+#pragma unroll
+            for (int i = 0; i < Cfg::SB1; ++i) {
+                const int e = tid + i * NT;
+                const int row = e / BK, kl = e % BK;
+                float v = 0.f;
+                if (e < BN * BK && n0 + row < p.N && k0 + kl < p.K) v = __ldg(B + (long long)(n0 + row) * p.K + k0 + kl);
+                rb[i] = v;
+            }
+        }
+    };
+    auto sstore = [&](int buf) {
+        float* as = As + buf * BK * LDA;
+        float* bs = Bs + buf * BK * LDB;
+        if (p.vec4) {
+            constexpr int KV = BK / 4;
+#pragma unroll
+            for (int i = 0; i < Cfg::SA4; ++i) {
+                const int e = tid + i * NT;
+                if (e < BM * KV) {
+                    const int row = e / KV, kl = (e % KV) * 4;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) as[(kl + j) * LDA + row] = ra[4 * i + j];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < Cfg::SB4; ++i) {
+                const int e = tid + i * NT;
+                if (e < BN * KV) {
+                    const int row = e / KV, kl = (e % KV) * 4;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) bs[(kl + j) * LDB + row] = rb[4 * i + j];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < Cfg::SA1; ++i) {
+                const int e = tid + i * NT;
+                if (e < BM * BK) as[(e % BK) * LDA + e / BK] = ra[i];
+            }
+#pragma unroll
+            for (int i = 0; i < Cfg::SB1; ++i) {
+                const int e = tid + i * NT;
+                if (e < BN * BK) bs[(e % BK) * LDB + e / BK] = rb[i];
+            }
+        }
+    };
+
+    gload(kt_begin);
+    sstore(0);
+    __syncthreads();
+    int buf = 0;
+    for (int kt = kt_begin; kt < kt_end; ++kt) {
+        const bool more = kt + 1 < kt_end;
+        if (more) gload(kt + 1);  // global loads in flight during the FMAs below
+        const float* as = As + buf * BK * LDA;
+        const float* bs = Bs + buf * BK * LDB;
+#pragma unroll UNROLL
+        for (int k = 0; k < BK; ++k) {
+            float a[TT], b[TT];
+            if constexpr (TT == 2) {
+                float2 va = *reinterpret_cast<const float2*>(as + k * LDA + ty * 2);
+                float2 vb = *reinterpret_cast<const float2*>(bs + k * LDB + tx * 2);
+                a[0] = va.x; a[1] = va.y; b[0] = vb.x; b[1] = vb.y;
+            } else {
+#pragma unroll
+                for (int g = 0; g < TT / 4; ++g) {
+                    float4 va = *reinterpret_cast<const float4*>(as + k * LDA + tile_row<BM, TT>(ty, 4 * g));
+                    float4 vb = *reinterpret_cast<const float4*>(bs + k * LDB + tile_row<BN, TT>(tx, 4 * g));
+                    a[4 * g + 0] = va.x; a[4 * g + 1] = va.y; a[4 * g + 2] = va.z; a[4 * g + 3] = va.w;
+                    b[4 * g + 0] = vb.x; b[4 * g + 1] = vb.y; b[4 * g + 2] = vb.z; b[4 * g + 3] = vb.w;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < TT; ++i)
+#pragma unroll
+                for (int j = 0; j < TT; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        if (more) {
+            sstore(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
+    }
+
+    // epilogue: direct stores (SPLIT_K = 1) or atomic partial-sum reduction
+    const bool atomic = p.split > 1;
+#pragma unroll
+    for (int i = 0; i < TT; ++i) {
+        const int m = m0 + tile_row<BM, TT>(ty, i);
+        if (m >= p.M) continue;
+        float* crow = C + (long long)m * p.N;
+#pragma unroll
+        for (int g = 0; g < (TT + 3) / 4; ++g) {
+            constexpr int W = TT < 4 ? TT : 4;
+            const int n = n0 + tile_row<BN, TT>(tx, W * g);
+            if (W == 4 && n + 3 < p.N && (p.N % 4) == 0) {
+                float4 v = make_float4(acc[i][4 * g], acc[i][4 * g + 1], acc[i][4 * g + 2], acc[i][4 * g + 3]);
+                if (atomic) atomicAdd(reinterpret_cast<float4*>(crow + n), v);
+                else *reinterpret_cast<float4*>(crow + n) = v;
+            } else if (W == 2 && n + 1 < p.N && (p.N % 2) == 0) {
+                float2 v = make_float2(acc[i][0], acc[i][1]);
+                if (atomic) atomicAdd(reinterpret_cast<float2*>(crow + n), v);
+                else *reinterpret_cast<float2*>(crow + n) = v;
+            } else {
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    if (n + j < p.N) {
+                        if (atomic) atomicAdd(crow + n + j, acc[i][W * g + j]);
+                        else crow[n + j] = acc[i][W * g + j];
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int BM, int BN, int BK, int TT, int UNROLL, bool CONV>
+cudaError_t simt_launch(const LaunchCtx& c) {
+    using Cfg = SimtCfg<BM, BN, BK, TT>;
+    auto kern = simt_gemm_f32_kernel<BM, BN, BK, TT, UNROLL, CONV>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    const ShapeInfo& s = *c.sh;
+    SimtParams p;
+    p.A = (const float*)c.x;
+    p.B = (const float*)c.w;
+    p.C = (float*)c.y;
+    p.M = (int)s.M; p.N = (int)s.N; p.K = (int)s.K;
+    p.sA = s.M * s.K; p.sB = s.N * s.K; p.sC = s.M * s.N;
+    p.ktiles = (int)((s.K + BK - 1) / BK);
+    p.split = c.split;
+    p.kt_per_split = (p.ktiles + c.split - 1) / c.split;
+    p.H = (int)s.h; p.W = (int)s.w; p.Cin = (int)s.c; p.P = (int)s.p; p.Q = (int)s.q; p.S = (int)s.s;
+    p.sh = s.sh; p.sw = s.sw; p.ph = s.ph; p.pw = s.pw; p.dh = s.dh; p.dw = s.dw;
+    p.vec4 = (BK % 4 == 0) && (CONV ? (s.c % 4 == 0) : (s.K % 4 == 0));
+    if (c.split > 1) {
+        cudaError_t e = cudaMemsetAsync(c.y, 0, (size_t)s.y_elems * sizeof(float), c.stream);
+        if (e != cudaSuccess) return e;
+    }
+    dim3 grid((unsigned)((s.M + BM - 1) / BM), (unsigned)((s.N + BN - 1) / BN), (unsigned)(s.batch * c.split));
+    kern<<<grid, Cfg::NT, Cfg::SMEM, c.stream>>>(p);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+template <int BM, int BN, int BK, int TT, int UNROLL, bool CONV>
+void simt_register() {
+    if constexpr (simt_static_ok(BM, BN, BK, TT)) {
+        registry_add(kernel_key(CONV ? SK_SIMT_IGEMM_CONV_F32 : SK_SIMT_GEMM_F32, BM, BN, BK, TT, UNROLL),
+                     &simt_launch<BM, BN, BK, TT, UNROLL, CONV>);
+    }
+}
+
+}  // namespace db200

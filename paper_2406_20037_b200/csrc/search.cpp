@@ -1,0 +1,574 @@
+// search.cpp — the host side of the hot path: knob-space encoding, the
+// Ansor-style sampler, sharded batch measurement with an all-gather, best-of-N
+// and Droplet Search.  Host-only C++; the GPU measurer lives in harness.cu.
+//
+// Paper: Def. 2.1, Example 2.3, neighbourhood
+// (P:290-294), Droplet Search, combined approach,
+// Droplet cap of 100 trials.  Readings R-xx: DESIGN.md §3.
+#include <chrono>
+#include <cstring>
+#include <limits>
+#include <unordered_set>
+
+#include "internal.hpp"
+
+namespace db200 {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+tuner_status fail(tuner_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+// ---------------------------------------------------------------- encoding (R-T1)
+uint64_t Tuner::linear(const Pt& p) const {
+    const SketchSpace& s = spaces[p.pos];
+    uint64_t lin = 0;
+    for (int d = 0; d < s.nknobs(); ++d) lin = lin * s.values[d].size() + (uint64_t)p.idx[d];
+    return s.offset + lin;
+}
+
+Pt Tuner::from_public(const tuner_point& tp, tuner_status& st) const {
+    Pt p;
+    st = TUNER_OK;
+    int pos = -1;
+    for (size_t i = 0; i < spaces.size(); ++i)
+        if (spaces[i].sketch == tp.sketch) { pos = (int)i; break; }
+    if (pos < 0) { st = fail(TUNER_ERANGE, "point's sketch is not in this tuner's spaces"); return p; }
+    const SketchSpace& s = spaces[pos];
+    if (tp.n != s.nknobs()) { st = fail(TUNER_EDIM, "index vector length != number of knobs"); return p; }
+    p.pos = pos;
+    p.n = tp.n;
+    for (int d = 0; d < tp.n; ++d) {
+        if (tp.idx[d] < 0 || tp.idx[d] >= (int32_t)s.values[d].size()) {
+            st = fail(TUNER_ERANGE, "index out of range");
+            return p;
+        }
+        p.idx[d] = tp.idx[d];
+    }
+    return p;
+}
+
+tuner_point Tuner::to_public(const Pt& p) const {
+    tuner_point tp;
+    std::memset(&tp, 0, sizeof(tp));
+    tp.sketch = spaces[p.pos].sketch;
+    tp.n = p.n;
+    for (int d = 0; d < p.n; ++d) tp.idx[d] = p.idx[d];
+    return tp;
+}
+
+void Tuner::values_of(const Pt& p, int32_t* v) const {
+    const SketchSpace& s = spaces[p.pos];
+    for (int d = 0; d < p.n; ++d) v[d] = s.values[d][p.idx[d]];
+}
+
+// Neighbourhood: one index step along one coordinate; no diagonals
+// (R-D7); out-of-range skipped, no wrap (R-D6); dimension-major, minus before
+// plus (R-D3).
+void Tuner::ring(const Pt& x, std::vector<Pt>& out) const {
+    out.clear();
+    const SketchSpace& s = spaces[x.pos];
+    for (int d = 0; d < x.n; ++d) {
+        for (int delta = -1; delta <= 1; delta += 2) {
+            int i = x.idx[d] + delta;
+            if (i < 0 || i >= (int)s.values[d].size()) continue;
+            Pt q = x;
+            q.idx[d] = i;
+            out.push_back(q);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- sharded measurement (R-M1)
+namespace {
+struct Slot {  // 32 bytes, keyed by batch index so results are rank-independent
+    int32_t idx;
+    int32_t status;
+    double cost_ns;
+    double max_err;
+    int32_t rank;
+    int32_t pad;
+};
+static_assert(sizeof(Slot) == 32, "slot layout");
+}  // namespace
+
+tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
+    if (batch.empty()) return TUNER_OK;
+    auto t0 = std::chrono::steady_clock::now();
+    const int G = opts.world > 1 ? opts.world : 1;
+    const int r = opts.world > 1 ? opts.rank : 0;
+    std::vector<Pt> local;
+    std::vector<int32_t> local_idx;
+    for (size_t j = r; j < batch.size(); j += G) {
+        local.push_back(batch[j]);
+        local_idx.push_back((int32_t)j);
+    }
+    std::vector<Result> lres;
+    const int64_t launches0 = g_launch_counter_ptr()->load();
+    tuner_status st = measurer->measure(local, lres);
+    stats.kernel_launches += g_launch_counter_ptr()->load() - launches0;
+    if (st != TUNER_OK) return st;
+    for (auto& x : lres) x.rank = r;
+    std::vector<Result> res(batch.size());
+    if (G == 1) {
+        res = lres;
+    } else {
+        const size_t per = (batch.size() + G - 1) / G;
+        std::vector<Slot> send(per), recv(per * G);
+        for (size_t i = 0; i < per; ++i) {
+            send[i] = Slot{-1, 0, 0.0, 0.0, r, 0};
+            if (i < lres.size())
+                send[i] = Slot{local_idx[i], lres[i].status, lres[i].cost_ns, lres[i].max_err, r, 0};
+        }
+        if (!comm) return fail(TUNER_ENCCL, "world > 1 but no communicator");
+        st = comm->allgather(send.data(), recv.data(), (int64_t)(per * sizeof(Slot)));
+        if (st != TUNER_OK) return st;
+        stats.collectives++;
+        size_t filled = 0;
+        for (const Slot& s : recv) {
+            if (s.idx < 0) continue;
+            if ((size_t)s.idx >= batch.size()) return fail(TUNER_ENCCL, "corrupt all-gather slot");
+            res[s.idx] = Result{s.cost_ns, s.max_err, s.status, s.rank};
+            ++filled;
+        }
+        if (filled != batch.size()) return fail(TUNER_ENCCL, "all-gather returned an incomplete batch");
+    }
+    for (size_t j = 0; j < batch.size(); ++j) {
+        tuner_result smp;
+        std::memset(&smp, 0, sizeof(smp));
+        smp.pt = to_public(batch[j]);
+        smp.status = res[j].status;
+        smp.cost_ns = res[j].status == TUNER_S_OK ? res[j].cost_ns : INFINITY;
+        smp.max_err = res[j].max_err;
+        smp.rank = res[j].rank;
+        memo[linear(batch[j])] = history.size();
+        history.push_back(smp);
+    }
+    stats.candidates += (int64_t)batch.size();
+    stats.batches++;
+    stats.measure_wall_ns +=
+        std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count();
+    return TUNER_OK;
+}
+
+// ---------------------------------------------------------------- sampler (R-S1)
+tuner_status Tuner::draw(int32_t n, std::vector<Pt>& out) {
+    out.clear();
+    std::unordered_set<uint64_t> taken;
+    int64_t attempts = 0;
+    const int64_t cap = 64ll * n;
+    while ((int32_t)out.size() < n && attempts < cap) {
+        ++attempts;
+        Pt p;
+        p.pos = (int32_t)rng.uniform((uint32_t)spaces.size());
+        const SketchSpace& s = spaces[p.pos];
+        p.n = s.nknobs();
+        for (int d = 0; d < p.n; ++d) p.idx[d] = (int32_t)rng.uniform((uint32_t)s.values[d].size());
+        if (!valid(p)) continue;
+        uint64_t id = linear(p);
+        if (memo.count(id) || taken.count(id)) continue;
+        taken.insert(id);
+        out.push_back(p);
+    }
+    return TUNER_OK;
+}
+
+// ---------------------------------------------------------------- Droplet Search
+// P:297-304.  Step 2(a) "If there exists c_i' ... yields a faster kernel ...
+// update the current best": the whole ring is measured as one batch and the
+// first strictly better argmin in ring order is taken (R-D2, R-D3, R-D4).
+// Step 2(b) "If there is no such c_i', then the search terminates."
+// GROW (R-D9): after a ring move along u, probe x_prev + 2^j u (j >= 1, clamped
+// until the clamp repeats) as one batch; accept ray points in order while each
+// is strictly better.  Budget counts new measurements incl. an unmeasured
+// start (R-D14); a truncated batch ends the search unconverged (R-D13).
+tuner_status Tuner::droplet(const Pt& start, int32_t budget, std::vector<Pt>& traj,
+                            tuner_droplet_report& rep) {
+    int32_t used = 0, rounds = 0;
+    tuner_status st;
+    if (!measured(start)) {
+        st = measure_batch(std::vector<Pt>{start});
+        if (st != TUNER_OK) return st;
+        used = 1;
+    }
+    Pt x = start;
+    double c = cost(x);
+    traj.assign(1, x);
+    auto finish = [&](bool converged) {
+        std::memset(&rep, 0, sizeof(rep));
+        rep.best = to_public(x);
+        rep.best_cost = c;
+        rep.trials_used = used;
+        rep.rounds = rounds;
+        rep.converged = converged ? 1 : 0;
+        rep.traj_len = (int32_t)traj.size();
+        return TUNER_OK;
+    };
+    // the not-yet-measured valid points of `cands`, truncated to the budget left
+    auto fresh = [&](const std::vector<Pt>& cands, std::vector<Pt>& q) {
+        q.clear();
+        size_t n = 0;
+        for (const Pt& p : cands) {
+            if (measured(p) || !valid(p)) continue;
+            ++n;
+            if ((int32_t)q.size() < budget - used) q.push_back(p);
+        }
+        return n > q.size();
+    };
+    std::vector<Pt> nb, q, ray;
+    for (;;) {
+        ring(x, nb);
+        bool trunc = fresh(nb, q);
+        if (!q.empty() && (st = measure_batch(q)) != TUNER_OK) return st;
+        used += (int32_t)q.size();
+        ++rounds;
+        int bi = -1;
+        double bc = 0.0;
+        for (size_t i = 0; i < nb.size(); ++i) {
+            if (!measured(nb[i]) || !valid(nb[i])) continue;
+            double cp = cost(nb[i]);
+            if (bi < 0 || cp < bc) { bi = (int)i; bc = cp; }
+        }
+        if (bi < 0 || !(bc < c)) return finish(!trunc);
+        const Pt prev = x;
+        x = nb[bi];
+        c = bc;
+        traj.push_back(x);
+        if (used == budget) return finish(false);
+        if (opts.policy != TUNER_DS_GROW) continue;
+        int d = 0;
+        while (x.idx[d] == prev.idx[d]) ++d;
+        const int step = x.idx[d] - prev.idx[d];
+        const int card = (int)spaces[x.pos].values[d].size();
+        ray.clear();
+        Pt last = x;
+        for (int64_t j = 1, span = 2;; ++j, span *= 2) {
+            int64_t i = (int64_t)prev.idx[d] + step * span;
+            if (i < 0) i = 0;
+            if (i > card - 1) i = card - 1;
+            Pt qj = x;
+            qj.idx[d] = (int32_t)i;
+            if (qj == last) break;
+            ray.push_back(qj);
+            last = qj;
+        }
+        trunc = fresh(ray, q);
+        if (!q.empty() && (st = measure_batch(q)) != TUNER_OK) return st;
+        used += (int32_t)q.size();
+        ++rounds;
+        for (const Pt& p : ray) {
+            if (measured(p) && valid(p) && cost(p) < c) {
+                x = p;
+                c = cost(p);
+                traj.push_back(x);
+            } else {
+                break;
+            }
+        }
+        if (trunc) return finish(false);
+    }
+}
+
+// ---------------------------------------------------------------- cost-table measurer
+namespace {
+struct TableMeasurer : Measurer {
+    Tuner* t;
+    std::vector<double> table;
+    TableMeasurer(Tuner* tt, std::vector<double>&& tab) : t(tt), table(std::move(tab)) {}
+    tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out) override {
+        out.resize(pts.size());
+        for (size_t i = 0; i < pts.size(); ++i) {
+            out[i] = Result{table[t->linear(pts[i])], 0.0, TUNER_S_OK, 0};
+        }
+        return TUNER_OK;
+    }
+    bool valid(const Pt& p) override { return std::isfinite(table[t->linear(p)]); }
+};
+
+struct CallbackComm : Comm {
+    tuner_allgather_fn fn;
+    void* ctx;
+    CallbackComm(tuner_allgather_fn f, void* c) : fn(f), ctx(c) {}
+    tuner_status allgather(const void* send, void* recv, int64_t bytes) override {
+        int rc = fn(ctx, send, recv, bytes);
+        return rc == 0 ? TUNER_OK : fail(TUNER_ENCCL, "host all-gather callback failed");
+    }
+};
+}  // namespace
+
+std::unique_ptr<Measurer> make_table_measurer(Tuner* t, std::vector<double>&& table) {
+    return std::unique_ptr<Measurer>(new TableMeasurer(t, std::move(table)));
+}
+
+std::unique_ptr<Comm> make_callback_comm(tuner_allgather_fn fn, void* ctx) {
+    return std::unique_ptr<Comm>(new CallbackComm(fn, ctx));
+}
+
+}  // namespace db200
+
+// ================================================================= C ABI
+using namespace db200;
+
+#define CHECK_HANDLE(t)                                                        \
+    do {                                                                       \
+        if (!(t)) return fail(TUNER_EINVAL, "NULL tuner handle");              \
+        if ((t)->dead) return fail(TUNER_ESTATE, "tuner handle is dead after a CUDA error"); \
+    } while (0)
+
+static tuner_status after(Tuner* t, tuner_status st) {
+    if (st == TUNER_ECUDA) t->dead = true;
+    return st;
+}
+
+extern "C" void tuner_opts_default(tuner_opts* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->warmup = 2;
+    o->repeats = 10;
+    o->number = 0;
+    o->timeout_ms = 1000.0;
+    o->seed = 0;
+    o->policy = TUNER_DS_GROW;
+    o->alpha = 0.0;
+    o->max_batch = 512;
+    o->verify = 1;
+    o->rank = 0;
+    o->world = 1;
+}
+
+extern "C" const char* tuner_last_error(void) { return g_err.c_str(); }
+
+extern "C" tuner_status tuner_create(int32_t op, const tuner_shape* shape, const tuner_knob_space* spaces,
+                                     int32_t nspaces, const tuner_opts* opts, tuner_t** out) {
+    if (!out) return fail(TUNER_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!shape || !spaces || nspaces < 1 || !opts) return fail(TUNER_EINVAL, "shape/spaces/opts missing");
+    std::unique_ptr<tuner> t(new tuner());
+    t->op = op;
+    t->shape = *shape;
+    t->opts = *opts;
+    if (t->opts.repeats < 1 || t->opts.warmup < 0 || t->opts.number < 0 || t->opts.max_batch < 1)
+        return fail(TUNER_EINVAL, "repeats >= 1, warmup >= 0, number >= 0, max_batch >= 1 required");
+    if (t->opts.alpha != 0.0) return fail(TUNER_EINVAL, "only alpha = 0 (strict median compare) is supported");
+    if (t->opts.policy != TUNER_DS_PLAIN && t->opts.policy != TUNER_DS_GROW)
+        return fail(TUNER_EINVAL, "unknown Droplet policy");
+    if (t->opts.world < 1) t->opts.world = 1;
+    if (t->opts.rank < 0 || t->opts.rank >= t->opts.world) return fail(TUNER_EINVAL, "rank out of range");
+    t->table_mode = opts->cost_table != nullptr;
+    std::string why;
+    if (!make_shape_info(op, *shape, t->info, why)) {
+        if (!t->table_mode) return fail(TUNER_EINVAL, why);
+    }
+    uint64_t off = 0;
+    for (int32_t i = 0; i < nspaces; ++i) {
+        const tuner_knob_space& ks = spaces[i];
+        if (ks.nknobs < 0 || ks.nknobs > TUNER_MAX_KNOBS || (ks.nknobs > 0 && (!ks.card || !ks.values)))
+            return fail(TUNER_EINVAL, "bad knob space");
+        for (int32_t j = 0; j < i; ++j)
+            if (spaces[j].sketch == ks.sketch) return fail(TUNER_EINVAL, "duplicate sketch id in spaces");
+        SketchSpace s;
+        s.sketch = ks.sketch;
+        const SketchDesc* desc = t->table_mode ? nullptr : sketch_desc(ks.sketch);
+        if (!t->table_mode) {
+            if (!desc) return fail(TUNER_ERANGE, "unknown sketch id");
+            if (!(desc->op_mask & (1 << op)) || desc->dtype != shape->dtype)
+                return fail(TUNER_EINVAL, std::string("sketch ") + desc->name + " does not implement this op/dtype");
+            if ((size_t)ks.nknobs != desc->values.size()) return fail(TUNER_EDIM, "knob count != sketch's knobs");
+        }
+        int32_t voff = 0;
+        unsigned __int128 size = 1;
+        for (int32_t d = 0; d < ks.nknobs; ++d) {
+            if (ks.card[d] < 1 || ks.card[d] > TUNER_MAX_VALUES) return fail(TUNER_EINVAL, "knob cardinality");
+            std::vector<int32_t> vals(ks.values + voff, ks.values + voff + ks.card[d]);
+            voff += ks.card[d];
+            for (size_t k = 1; k < vals.size(); ++k)
+                if (!(vals[k - 1] < vals[k])) return fail(TUNER_EINVAL, "knob values must be strictly increasing");
+            if (desc) {
+                for (int32_t v : vals) {
+                    bool ok = false;
+                    for (int32_t sv : desc->values[d]) ok |= (sv == v);
+                    if (!ok)
+                        return fail(TUNER_EINVAL, std::string("value ") + std::to_string(v) + " of knob " +
+                                                      desc->knob_names[d] + " is not compiled for " + desc->name);
+                }
+            }
+            s.values.push_back(std::move(vals));
+            size *= (unsigned __int128)ks.card[d];
+            if (size > ((unsigned __int128)1 << 62)) return fail(TUNER_EOVERFLOW, "space larger than 2^62");
+        }
+        s.size = (uint64_t)size;
+        s.offset = off;
+        off += s.size;
+        if (off > (1ull << 62)) return fail(TUNER_EOVERFLOW, "space larger than 2^62");
+        t->spaces.push_back(std::move(s));
+    }
+    t->total = off;
+    t->rng = SplitMix64(opts->seed);
+    if (t->opts.world > 1) {
+        if (opts->allgather) {
+            t->comm = make_callback_comm(opts->allgather, opts->allgather_ctx);
+        } else if (opts->nccl_unique_id) {
+            tuner_status st = make_nccl_comm(opts->nccl_unique_id, t->opts.rank, t->opts.world, opts->stream, t->comm);
+            if (st != TUNER_OK) return st;
+        } else {
+            return fail(TUNER_EINVAL, "world > 1 needs an allgather callback or an NCCL unique id");
+        }
+    }
+    if (t->table_mode) {
+        if ((uint64_t)opts->cost_table_len != t->total)
+            return fail(TUNER_EINVAL, "cost_table_len != total number of points");
+        std::vector<double> tab(opts->cost_table, opts->cost_table + opts->cost_table_len);
+        for (double v : tab)
+            if (std::isnan(v)) return fail(TUNER_EINVAL, "NaN in cost table");
+        t->measurer = make_table_measurer(t.get(), std::move(tab));
+    } else {
+        if (!opts->x || !opts->w || !opts->y) return fail(TUNER_EINVAL, "measured mode needs x, w, y device buffers");
+        tuner_status st = make_gpu_measurer(t.get(), t->measurer);
+        if (st != TUNER_OK) return st;
+    }
+    *out = t.release();
+    return TUNER_OK;
+}
+
+extern "C" tuner_status tuner_point_valid(const tuner_t* tc, const tuner_point* pt, int32_t* valid) {
+    Tuner* t = const_cast<tuner_t*>(tc);
+    CHECK_HANDLE(t);
+    if (!pt || !valid) return fail(TUNER_EINVAL, "NULL argument");
+    tuner_status st;
+    Pt p = t->from_public(*pt, st);
+    if (st != TUNER_OK) return st;
+    *valid = t->valid(p) ? 1 : 0;
+    return TUNER_OK;
+}
+
+static void fill_sample(Tuner* t, const Pt& p, tuner_result* out) { *out = t->history[t->memo.at(t->linear(p))]; }
+
+extern "C" tuner_status tuner_sample(tuner_t* t, int32_t n, tuner_result* out, int32_t* n_out) {
+    CHECK_HANDLE(t);
+    if (n < 0 || (n > 0 && !out) || !n_out) return fail(TUNER_EINVAL, "bad arguments");
+    *n_out = 0;
+    std::vector<Pt> pts;
+    t->draw(n, pts);
+    for (size_t i = 0; i < pts.size(); i += (size_t)t->opts.max_batch) {
+        size_t e = std::min(pts.size(), i + (size_t)t->opts.max_batch);
+        std::vector<Pt> b(pts.begin() + i, pts.begin() + e);
+        tuner_status st = t->measure_batch(b);
+        if (st != TUNER_OK) return after(t, st);
+    }
+    for (size_t i = 0; i < pts.size(); ++i) fill_sample(t, pts[i], &out[i]);
+    *n_out = (int32_t)pts.size();
+    return TUNER_OK;
+}
+
+extern "C" tuner_status tuner_measure(tuner_t* t, const tuner_point* pts, int32_t n, tuner_result* out) {
+    CHECK_HANDLE(t);
+    if (n < 0 || (n > 0 && (!pts || !out))) return fail(TUNER_EINVAL, "bad arguments");
+    std::vector<Pt> all(n), todo;
+    std::vector<char> ok(n, 0);
+    std::unordered_set<uint64_t> seen;
+    for (int32_t i = 0; i < n; ++i) {
+        tuner_status st;
+        all[i] = t->from_public(pts[i], st);
+        if (st != TUNER_OK) return st;
+        ok[i] = t->valid(all[i]);
+        uint64_t id = t->linear(all[i]);
+        if (ok[i] && !t->memo.count(id) && !seen.count(id)) {
+            seen.insert(id);
+            todo.push_back(all[i]);
+        }
+    }
+    for (size_t i = 0; i < todo.size(); i += (size_t)t->opts.max_batch) {
+        size_t e = std::min(todo.size(), i + (size_t)t->opts.max_batch);
+        tuner_status st = t->measure_batch(std::vector<Pt>(todo.begin() + i, todo.begin() + e));
+        if (st != TUNER_OK) return after(t, st);
+    }
+    for (int32_t i = 0; i < n; ++i) {
+        if (ok[i]) {
+            fill_sample(t, all[i], &out[i]);
+        } else {
+            std::memset(&out[i], 0, sizeof(out[i]));
+            out[i].pt = pts[i];
+            out[i].cost_ns = INFINITY;
+            out[i].status = TUNER_S_INVALID;
+            out[i].rank = -1;
+        }
+    }
+    return TUNER_OK;
+}
+
+extern "C" tuner_status tuner_droplet(tuner_t* t, const tuner_point* start, int32_t budget, tuner_point* traj,
+                                      int32_t traj_cap, tuner_droplet_report* report) {
+    CHECK_HANDLE(t);
+    if (!start || !report) return fail(TUNER_EINVAL, "NULL argument");
+    if (budget < 1) return fail(TUNER_EINVAL, "budget must be >= 1");
+    tuner_status st;
+    Pt s = t->from_public(*start, st);
+    if (st != TUNER_OK) return st;
+    if (!t->valid(s)) return fail(TUNER_ERANGE, "start point is statically invalid");
+    std::vector<Pt> tr;
+    st = t->droplet(s, budget, tr, *report);
+    if (st != TUNER_OK) return after(t, st);
+    if (traj)
+        for (int32_t i = 0; i < (int32_t)tr.size() && i < traj_cap; ++i) traj[i] = t->to_public(tr[i]);
+    return TUNER_OK;
+}
+
+extern "C" tuner_status tuner_best(const tuner_t* tc, tuner_result* out) {
+    Tuner* t = const_cast<tuner_t*>(tc);
+    CHECK_HANDLE(t);
+    if (!out) return fail(TUNER_EINVAL, "NULL out");
+    if (t->history.empty()) return fail(TUNER_ESTATE, "tuner_best before any measurement");
+    size_t bi = 0;
+    for (size_t i = 1; i < t->history.size(); ++i)
+        if (t->history[i].cost_ns < t->history[bi].cost_ns) bi = i;  // first argmin (R-B1)
+    *out = t->history[bi];
+    return TUNER_OK;
+}
+
+extern "C" tuner_status tuner_history(const tuner_t* tc, tuner_result* out, int64_t cap, int64_t* n_out) {
+    Tuner* t = const_cast<tuner_t*>(tc);
+    if (!t) return fail(TUNER_EINVAL, "NULL tuner handle");
+    if (!n_out) return fail(TUNER_EINVAL, "NULL n_out");
+    *n_out = (int64_t)t->history.size();
+    if (out)
+        for (int64_t i = 0; i < cap && i < (int64_t)t->history.size(); ++i) out[i] = t->history[i];
+    return TUNER_OK;
+}
+
+extern "C" tuner_status tuner_get_stats(const tuner_t* tc, tuner_stats* out) {
+    if (!tc || !out) return fail(TUNER_EINVAL, "NULL argument");
+    *out = tc->stats;
+    return TUNER_OK;
+}
+
+extern "C" tuner_status kernel_run(const tuner_t* tc, const tuner_point* cfg, const tuner_buffers* buf, void* stream) {
+    Tuner* t = const_cast<tuner_t*>(tc);
+    CHECK_HANDLE(t);
+    if (!cfg || !buf) return fail(TUNER_EINVAL, "NULL argument");
+    if (t->table_mode) return fail(TUNER_ESTATE, "kernel_run in cost-table mode");
+    tuner_status st;
+    Pt p = t->from_public(*cfg, st);
+    if (st != TUNER_OK) return st;
+    if (!t->valid(p)) return fail(TUNER_ERANGE, "statically invalid schedule");
+    return after(t, gpu_kernel_run(t, p, buf, stream ? stream : t->opts.stream));
+}
+
+extern "C" tuner_status tuner_reference(const tuner_t* tc, const tuner_buffers* buf, float* y_ref, float* y_absref,
+                                        void* stream) {
+    Tuner* t = const_cast<tuner_t*>(tc);
+    CHECK_HANDLE(t);
+    if (!buf || !y_ref || !y_absref) return fail(TUNER_EINVAL, "NULL argument");
+    if (t->table_mode) return fail(TUNER_ESTATE, "tuner_reference in cost-table mode");
+    return after(t, gpu_reference(t, buf, y_ref, y_absref, stream ? stream : t->opts.stream));
+}
+
+extern "C" tuner_status tuner_nccl_unique_id(void* out128) {
+    if (!out128) return fail(TUNER_EINVAL, "NULL out");
+    return nccl_unique_id(out128);
+}
+
+extern "C" void tuner_destroy(tuner_t* t) { delete t; }
+
+extern "C" int64_t tuner_global_launch_count(void) { return g_launch_counter_ptr()->load(); }

@@ -1,0 +1,24 @@
+// shape.hpp — sketch ids and the GEMM view of a problem (kernel-side header).
+#pragma once
+#include <cstdint>
+
+namespace db200 {
+
+enum SketchId : int32_t {
+    SK_SIMT_GEMM_F32 = 0,
+    SK_SIMT_IGEMM_CONV_F32 = 1,
+    SK_TC_GEMM_BF16 = 2,
+    SK_TC_IGEMM_CONV_BF16 = 3,
+    SK_COUNT = 4
+};
+
+struct ShapeInfo {  // derived GEMM view of the problem
+    int32_t op, dtype;
+    int64_t batch, M, N, K;     // GEMM: Y[batch][M][N] = A[batch][M][K] * B[batch][N][K]^T
+    // conv
+    int64_t n, h, w, c, k, r, s, p, q;
+    int32_t sh, sw, ph, pw, dh, dw;
+    int64_t y_elems, x_elems, w_elems;
+};
+
+}  // namespace db200

@@ -1,0 +1,177 @@
+// sketches.cpp — the sketch catalogue (Def. 2.1: a sketch is a fixed
+// sequence of transformations; its annotations are the knobs) and the static
+// validity rules (sketch rules are hardware-dependent; P:596-599:
+// schedules that exceed thread limits are invalid).  Host-only.
+#include <algorithm>
+
+#include "internal.hpp"
+
+namespace db200 {
+
+static std::vector<SketchDesc> build_catalogue() {
+    std::vector<SketchDesc> c;
+    // SIMT fp32 GEMM family: block tile BM x BN, K step BK, TT x TT register tile
+    // per thread, inner-k UNROLL, split-K (runtime; partial sums reduced with
+    // vector atomics into a zeroed Y).
+    const std::vector<const char*> simt_names = {"BM", "BN", "BK", "TT", "UNROLL", "SPLIT_K"};
+    const std::vector<std::vector<int32_t>> simt_vals = {
+        {16, 32, 64, 128}, {16, 32, 64, 128}, {4, 8, 16, 32}, {2, 4, 8}, {1, 2, 4, 8}, {1, 2, 4, 8, 16}};
+    c.push_back({SK_SIMT_GEMM_F32, "simt_gemm_f32", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL),
+                 TUNER_F32, simt_names, simt_vals});
+    c.push_back({SK_SIMT_IGEMM_CONV_F32, "simt_igemm_conv_f32", 1 << TUNER_OP_CONV2D, TUNER_F32, simt_names,
+                 simt_vals});
+    // tcgen05 bf16 GEMM family: UMMA tile BM x BN (accumulator in TMEM), K step
+    // BK staged by TMA with 128-byte swizzle, STAGES-deep mbarrier pipeline,
+    // split-K (runtime).
+    const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K"};
+    const std::vector<std::vector<int32_t>> tc_vals = {{128}, {64, 128, 256}, {64}, {2, 3, 4, 6}, {1, 2, 4}};
+    c.push_back({SK_TC_GEMM_BF16, "tc_gemm_bf16", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL), TUNER_BF16,
+                 tc_names, tc_vals});
+    c.push_back({SK_TC_IGEMM_CONV_BF16, "tc_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tc_names, tc_vals});
+    return c;
+}
+
+static const std::vector<SketchDesc>& catalogue() {
+    static const std::vector<SketchDesc> c = build_catalogue();
+    return c;
+}
+
+const SketchDesc* sketch_desc(int32_t id) {
+    for (const auto& d : catalogue())
+        if (d.id == id) return &d;
+    return nullptr;
+}
+
+bool make_shape_info(int32_t op, const tuner_shape& s, ShapeInfo& o, std::string& why) {
+    o = ShapeInfo{};
+    o.op = op;
+    o.dtype = s.dtype;
+    if (s.dtype != TUNER_F32 && s.dtype != TUNER_BF16) { why = "unknown dtype"; return false; }
+    if (op == TUNER_OP_DENSE || op == TUNER_OP_BATCH_MATMUL) {
+        o.batch = op == TUNER_OP_DENSE ? 1 : s.b;
+        o.M = s.m; o.N = s.n; o.K = s.k;
+        if (o.batch < 1 || o.M < 1 || o.N < 1 || o.K < 1) { why = "b, m, n, k must be >= 1"; return false; }
+        o.x_elems = o.batch * o.M * o.K;
+        o.w_elems = o.batch * o.N * o.K;
+        o.y_elems = o.batch * o.M * o.N;
+        return true;
+    }
+    if (op != TUNER_OP_CONV2D) { why = "unknown op"; return false; }
+    if (s.N < 1 || s.C < 1 || s.H < 1 || s.W < 1 || s.K < 1 || s.R < 1 || s.S < 1) {
+        why = "conv N, C, H, W, K, R, S must be >= 1"; return false;
+    }
+    if (s.stride_h < 1 || s.stride_w < 1 || s.dil_h < 1 || s.dil_w < 1 || s.pad_h < 0 || s.pad_w < 0) {
+        why = "stride/dilation must be >= 1 and padding >= 0"; return false;
+    }
+    o.n = s.N; o.h = s.H; o.w = s.W; o.c = s.C; o.k = s.K; o.r = s.R; o.s = s.S;
+    o.sh = s.stride_h; o.sw = s.stride_w; o.ph = s.pad_h; o.pw = s.pad_w; o.dh = s.dil_h; o.dw = s.dil_w;
+    o.p = (s.H + 2 * s.pad_h - s.dil_h * (s.R - 1) - 1) / s.stride_h + 1;
+    o.q = (s.W + 2 * s.pad_w - s.dil_w * (s.S - 1) - 1) / s.stride_w + 1;
+    if (o.p < 1 || o.q < 1) { why = "empty conv output"; return false; }
+    o.batch = 1;
+    o.M = o.n * o.p * o.q;
+    o.N = o.k;
+    o.K = o.r * o.s * o.c;
+    o.x_elems = o.n * o.h * o.w * o.c;
+    o.w_elems = o.k * o.r * o.s * o.c;
+    o.y_elems = o.M * o.N;
+    if (o.M >= (1ll << 31) || o.K >= (1ll << 31) || o.N >= (1ll << 31)) { why = "problem too large"; return false; }
+    return true;
+}
+
+// SIMT: vector width the kernel will use for global loads (128-bit when the
+// reduction run allows it, R-K2).
+int simt_vec(const ShapeInfo& sh, int bk) {
+    if (bk % 4) return 1;
+    if (sh.op == TUNER_OP_CONV2D) return (sh.c % 4 == 0) ? 4 : 1;
+    return (sh.K % 4 == 0) ? 4 : 1;
+}
+
+static bool simt_valid(const ShapeInfo& sh, const int32_t* v) {
+    const int bm = v[0], bn = v[1], bk = v[2], tt = v[3], split = v[5];
+    if (sh.dtype != TUNER_F32) return false;
+    if (tt > bm || tt > bn) return false;
+    const int threads = (bm / tt) * (bn / tt);
+    if (threads > 1024 || threads < 1) return false;
+    const int vec = simt_vec(sh, bk);
+    const int la = (bm * bk / vec + threads - 1) / threads;  // A vectors staged per thread
+    const int lb = (bn * bk / vec + threads - 1) / threads;
+    if ((la + lb) * vec > 64) return false;  // register budget for the staging buffers
+    const int64_t ktiles = (sh.K + bk - 1) / bk;
+    if (split > ktiles) return false;  // empty K slices
+    const int64_t ntiles = (sh.N + bn - 1) / bn;
+    if (ntiles > 65535 || (int64_t)split * sh.batch > 65535) return false;
+    return true;
+}
+
+static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
+    const int bm = v[0], bn = v[1], bk = v[2], stages = v[3], split = v[4];
+    if (sh.dtype != TUNER_BF16) return false;
+    // TMA needs 16-byte aligned global strides: K (bf16) multiple of 8.
+    if (sh.op == TUNER_OP_CONV2D) {
+        if (sh.c % 8) return false;
+    } else if (sh.K % 8) {
+        return false;
+    }
+    const int64_t smem = (int64_t)stages * (bm + bn) * bk * 2 + 1024 /*align*/ + 256 /*barriers*/;
+    if (smem > 227 * 1024) return false;
+    if (bn > 256 || bm != 128) return false;
+    const int64_t ktiles = (sh.K + bk - 1) / bk;
+    if (split > ktiles) return false;
+    if ((int64_t)split * sh.batch > 65535) return false;
+    return true;
+}
+
+bool sketch_valid(int32_t id, const ShapeInfo& sh, const int32_t* v) {
+    const SketchDesc* d = sketch_desc(id);
+    if (!d || !(d->op_mask & (1 << sh.op)) || d->dtype != sh.dtype) return false;
+    switch (id) {
+        case SK_SIMT_GEMM_F32:
+        case SK_SIMT_IGEMM_CONV_F32: return simt_valid(sh, v);
+        case SK_TC_GEMM_BF16:
+        case SK_TC_IGEMM_CONV_BF16: return tc_valid(sh, v);
+        default: return false;
+    }
+}
+
+}  // namespace db200
+
+// ---------------------------------------------------------------- C ABI (catalogue)
+using namespace db200;
+
+extern "C" tuner_status tuner_sketches(int32_t op, int32_t dtype, int32_t* ids, int32_t cap, int32_t* n_out) {
+    if (!n_out) return fail(TUNER_EINVAL, "n_out is NULL");
+    int32_t n = 0;
+    for (const auto& d : catalogue()) {
+        if ((d.op_mask & (1 << op)) && d.dtype == dtype) {
+            if (ids && n < cap) ids[n] = d.id;
+            ++n;
+        }
+    }
+    *n_out = n;
+    return TUNER_OK;
+}
+
+extern "C" tuner_status tuner_sketch_space(int32_t sketch, int32_t* nknobs, int32_t* card, int32_t* values) {
+    const SketchDesc* d = sketch_desc(sketch);
+    if (!d) return fail(TUNER_ERANGE, "unknown sketch id");
+    if (!nknobs || !card || !values) return fail(TUNER_EINVAL, "NULL output");
+    *nknobs = (int32_t)d->values.size();
+    int32_t off = 0;
+    for (size_t i = 0; i < d->values.size(); ++i) {
+        card[i] = (int32_t)d->values[i].size();
+        for (int32_t v : d->values[i]) values[off++] = v;
+    }
+    return TUNER_OK;
+}
+
+extern "C" const char* tuner_sketch_name(int32_t sketch) {
+    const SketchDesc* d = sketch_desc(sketch);
+    return d ? d->name : nullptr;
+}
+
+extern "C" const char* tuner_knob_name(int32_t sketch, int32_t knob) {
+    const SketchDesc* d = sketch_desc(sketch);
+    if (!d || knob < 0 || knob >= (int32_t)d->knob_names.size()) return nullptr;
+    return d->knob_names[knob];
+}

@@ -1,0 +1,60 @@
+"""The C-ABI library loads without a GPU and exports every symbol include/*.h
+declares; the catalogue answers; the Python binding mirrors the header."""
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+from paper_2406_20037_b200 import _lib as L
+from paper_2406_20037_b200 import knob_names, sketch_name, sketch_space, sketches
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*([a-z_0-9]+)\s*\(", src, re.M):
+            names.add(m.group(1))
+    names -= {"if", "int", "typedef"}
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(L.LIB_PATH)
+    names = declared_functions()
+    assert len(names) >= 19
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+    assert names <= set(L.SIGNATURES), sorted(names - set(L.SIGNATURES))
+
+
+def test_struct_sizes_match_c_layout():
+    assert ctypes.sizeof(L.Point) == 72
+    assert ctypes.sizeof(L.Result) == 96
+    assert ctypes.sizeof(L.Shape) == 4 + 4 + 11 * 8 + 6 * 4
+
+
+def test_catalogue():
+    assert sketches("dense", "f32") == [0]
+    assert sketches("batch_matmul", "f32") == [0]
+    assert sketches("conv2d", "f32") == [1]
+    assert sketches("dense", "bf16") == [2]
+    assert sketch_name(0) == "simt_gemm_f32"
+    assert knob_names(0) == ["BM", "BN", "BK", "TT", "UNROLL", "SPLIT_K"]
+    sp = sketch_space(0)
+    assert sp[0] == [16, 32, 64, 128] and sp[5] == [1, 2, 4, 8, 16]
+    assert sketch_name(99) is None
+
+
+def test_measured_mode_rejects_uncompiled_values():
+    import torch
+    from paper_2406_20037_b200 import Tuner, TunerError
+    x = torch.zeros(4)
+    with pytest.raises(TunerError, match="EINVAL"):
+        Tuner("dense", {"m": 4, "n": 4, "k": 4}, spaces=[(0, [[24], [16], [4], [4], [1], [1]])], x=x, w=x, y=x,
+              stream=0)

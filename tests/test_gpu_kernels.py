@@ -1,0 +1,183 @@
+"""GPU parity: every sketch's outputs vs the oracle (element by element), the
+library's naive reference vs the oracle, and the measurement harness end to
+end.  Run on a B200 via gpurun (-m gpu)."""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import contractions as oc
+from oracle import numerics as on
+from paper_2406_20037_b200 import Tuner, global_launch_count, sketch_space
+from synth import tensors
+
+pytestmark = pytest.mark.gpu
+
+
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch.device("cuda:0")
+
+
+def all_points(sketch):
+    vals = sketch_space(sketch)
+    import itertools
+    return [(sketch, idx) for idx in itertools.product(*[range(len(v)) for v in vals])]
+
+
+def to_dev(*arrs):
+    return [torch.from_numpy(np.ascontiguousarray(a)).to(dev()) for a in arrs]
+
+
+def gemm_case(b, m, n, k, dist, seed):
+    x, w = tensors([(b, m, k), (b, n, k)], seed, dist)
+    yo, ao = oc.bmm(x, w)
+    return x, w, yo, ao
+
+
+def run_points(t, pts, x, w, y):
+    outs = []
+    for p in pts:
+        y.fill_(float("nan"))
+        t.run(p, x, w, y)
+        torch.cuda.synchronize()
+        outs.append((p, y.cpu().numpy().copy()))
+    return outs
+
+
+@pytest.mark.parametrize("shape", [(1, 75, 53, 37), (1, 64, 96, 36), (3, 33, 17, 130), (1, 128, 128, 64)])
+def test_simt_gemm_all_configs_vs_oracle(shape):
+    b, m, n, k = shape
+    op = "dense" if b == 1 else "batch_matmul"
+    x, w, yo, ao = gemm_case(b, m, n, k, "uniform", sum(shape))
+    xd, wd = to_dev(x, w)
+    y = torch.empty(b, m, n, device=dev())
+    t = Tuner(op, {"b": b, "m": m, "n": n, "k": k}, spaces=[(0, sketch_space(0))], x=xd, w=wd, y=y)
+    pts = [p for p in all_points(0) if t.valid(p)]
+    rng = random.Random(0)
+    sel = pts if len(pts) <= 700 else rng.sample(pts, 700)
+    bad = []
+    for p, yv in run_points(t, sel, xd, wd, y):
+        e = on.max_rel_err(yv.reshape(yo.shape), yo, ao)
+        if not e <= on.TOL_F32:
+            bad.append((p, t.values(p), e))
+    assert not bad, bad[:5]
+    assert len(sel) > 100
+
+
+def test_simt_gemm_exact_integer_inputs():
+    b, m, n, k = 1, 70, 45, 92
+    x, w, yo, _ = gemm_case(b, m, n, k, "int", 5)
+    xd, wd = to_dev(x, w)
+    y = torch.empty(b, m, n, device=dev())
+    t = Tuner("dense", {"m": m, "n": n, "k": k}, spaces=[(0, sketch_space(0))], x=xd, w=wd, y=y)
+    pts = [p for p in all_points(0) if t.valid(p)]
+    for p, yv in run_points(t, random.Random(1).sample(pts, 200), xd, wd, y):
+        np.testing.assert_array_equal(yv.reshape(yo.shape), yo.astype(np.float32), err_msg=str(t.values(p)))
+
+
+CONV_CASES = [
+    # N, H, W, C, K, R, S, stride, pad, dil
+    (1, 13, 11, 3, 10, 3, 3, (1, 1), (1, 1), (1, 1)),
+    (2, 9, 9, 8, 20, 3, 3, (2, 2), (1, 1), (1, 1)),
+    (1, 15, 15, 3, 16, 7, 7, (2, 2), (3, 3), (1, 1)),
+    (1, 10, 12, 12, 9, 1, 1, (2, 2), (0, 0), (1, 1)),
+    (1, 11, 10, 4, 6, 3, 2, (1, 2), (2, 0), (2, 1)),
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_simt_igemm_conv_vs_oracle(case):
+    n, h, wd_, c, k, r, s, st, pd, dl = case
+    x, w = tensors([(n, h, wd_, c), (k, r, s, c)], sum(case[:7]))
+    yo, ao = oc.conv2d(x, w, st, pd, dl)
+    xd, wdd = to_dev(x, w)
+    y = torch.empty(yo.shape, device=dev())
+    shape = {"N": n, "H": h, "W": wd_, "C": c, "K": k, "R": r, "S": s, "stride": st, "pad": pd, "dil": dl}
+    t = Tuner("conv2d", shape, spaces=[(1, sketch_space(1))], x=xd, w=wdd, y=y)
+    pts = [p for p in all_points(1) if t.valid(p)]
+    bad = []
+    for p, yv in run_points(t, random.Random(2).sample(pts, min(300, len(pts))), xd, wdd, y):
+        e = on.max_rel_err(yv, yo, ao)
+        if not e <= on.TOL_F32:
+            bad.append((t.values(p), e))
+    assert not bad, bad[:5]
+
+
+def test_naive_reference_vs_oracle():
+    x, w = tensors([(2, 10, 9, 5), (7, 3, 3, 5)], 3)
+    yo, ao = oc.conv2d(x, w, (2, 1), (1, 1))
+    xd, wd = to_dev(x, w)
+    y = torch.empty(yo.shape, device=dev())
+    shape = {"N": 2, "H": 10, "W": 9, "C": 5, "K": 7, "R": 3, "S": 3, "stride": (2, 1), "pad": (1, 1)}
+    t = Tuner("conv2d", shape, spaces=[(1, sketch_space(1))], x=xd, w=wd, y=y)
+    yr, ar = torch.empty_like(y), torch.empty_like(y)
+    t.reference(xd, wd, yr, ar)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(yr.cpu().numpy(), yo.astype(np.float32), rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(ar.cpu().numpy(), ao.astype(np.float32), rtol=1e-6)
+
+
+def test_harness_sample_droplet_and_replay():
+    from oracle.search import OracleTuner, Space
+    m = n = k = 256
+    x, w, yo, ao = gemm_case(1, m, n, k, "uniform", 11)
+    xd, wd = to_dev(x, w)
+    y = torch.empty(m, n, device=dev())
+    t = Tuner("dense", {"m": m, "n": n, "k": k}, x=xd, w=wd, y=y, seed=3)
+    l0 = global_launch_count()
+    smp = t.sample(64)
+    assert len(smp) == 64
+    assert all(s.status == "ok" and s.max_err <= 1e-4 and 0 < s.cost_ns < 1e8 for s in smp), smp[:3]
+    assert global_launch_count() - l0 >= 64 * (1 + 2 + 10)
+    pre = {(s.point[0], s.point[1]): s.cost_ns for s in t.history()}
+    b = t.best()
+    assert b.cost_ns == min(s.cost_ns for s in smp)
+    rep = t.droplet(b.point, 100)
+    assert rep["trials_used"] <= 100
+    log = {(s.point[0], s.point[1]): s.cost_ns for s in t.history()}
+    # record/replay: the oracle's Droplet over the logged costs
+    # reproduces the GPU trajectory and never asks for an unlogged point
+    sp = Space([sketch_space(0)])
+    to_o = lambda p: (0, p[1])
+
+    def cost(p):
+        return log[(0, p[1])]
+    ot = OracleTuner(sp, cost, lambda p: (0, p[1]) in log)
+    ot.measure([to_o(p) for p in pre])
+    orep = ot.droplet(to_o(b.point), 100, "grow")
+    assert [p[1] for p in orep["traj"]] == [p[1] for p in rep["traj"]]
+    assert orep["trials_used"] == rep["trials_used"] and orep["converged"] == rep["converged"]
+    # the chosen schedule really computes the layer
+    t.run(rep["best"], xd, wd, y)
+    torch.cuda.synchronize()
+    assert on.max_rel_err(y.cpu().numpy(), yo, ao) <= 1e-4
+
+
+def test_config1_bruteforce_and_droplet():
+    # BASELINE config 1: dense 512^3 fp32, 4-knob space (TT=4, SPLIT_K=1), 256 points, all valid
+    m = n = k = 512
+    x, w, yo, ao = gemm_case(1, m, n, k, "uniform", 0)
+    xd, wd = to_dev(x, w)
+    y = torch.empty(m, n, device=dev())
+    space = [[16, 32, 64, 128], [16, 32, 64, 128], [4, 8, 16, 32], [4], [1, 2, 4, 8], [1]]
+    import itertools
+    pts = [(0, idx) for idx in itertools.product(*[range(len(v)) for v in space])]
+    t = Tuner("dense", {"m": m, "n": n, "k": k}, spaces=[(0, space)], x=xd, w=wd, y=y, policy="grow")
+    assert all(t.valid(p) for p in pts) and len(pts) == 256
+    rep = t.droplet((0, (0, 0, 0, 0, 0, 0)), 100)
+    res = t.measure(pts)
+    assert all(r.status == "ok" for r in res)
+    cost = {r.point: r.cost_ns for r in res}
+    best_bf = min(cost.values())
+    # converged => local minimum under the paper's neighbourhood (measured costs)
+    if rep["converged"]:
+        sp_ring = []
+        for d in range(6):
+            for dlt in (-1, 1):
+                i = rep["best"][1][d] + dlt
+                if 0 <= i < len(space[d]):
+                    q = list(rep["best"][1]); q[d] = i; sp_ring.append((0, tuple(q)))
+        assert all(cost[q] >= rep["best_cost"] for q in sp_ring)
+    print(f"config1: droplet {rep['best_cost']:.0f} ns in {rep['trials_used']} trials; brute force {best_bf:.0f} ns")
