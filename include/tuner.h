@@ -125,6 +125,9 @@ typedef struct {
     double alpha;      /* 0: strict median compare (only value supported) */
     int32_t max_batch; /* candidates per measured batch / collective (default 512) */
     int32_t verify;    /* 1: verify every candidate (default), 0: skip */
+    double early_cut;  /* > 0: a candidate whose verify run is slower than early_cut x
+                          the best cost known so far is ranked by that run alone
+                          (no timed repeats; SURVEY d.5).  0 = off (default). */
     /* cost-table mode (R-T1): dense costs per sketch in linear-id order,
      * concatenated in the order of `spaces`; +inf = invalid; NaN -> EINVAL.
      * Copied at create; no device is touched in this mode. */

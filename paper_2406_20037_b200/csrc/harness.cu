@@ -125,7 +125,7 @@ struct GpuMeasurer : Measurer {
         return resolve(t, p, split) != nullptr;
     }
 
-    tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out) override {
+    tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out, double incumbent) override {
         const size_t n = pts.size();
         out.assign(n, Result{});
         if (n == 0) return TUNER_OK;
@@ -180,12 +180,22 @@ struct GpuMeasurer : Measurer {
             else if (ms > t->opts.timeout_ms) out[j].status = TUNER_S_TIMEOUT;
         }
 
+        // early cut (SURVEY d.5): rank hopeless candidates by their verify run
+        std::vector<char> cut(n, 0);
+        if (t->opts.early_cut > 0.0) {
+            double ref_ns = incumbent;
+            for (size_t j = 0; j < n; ++j)
+                if (out[j].status == TUNER_S_OK) ref_ns = std::min(ref_ns, tver[j]);
+            for (size_t j = 0; j < n; ++j)
+                if (out[j].status == TUNER_S_OK && tver[j] > t->opts.early_cut * ref_ns) cut[j] = 1;
+        }
+
         // ---- phase 2: timing
         std::vector<cudaGraphExec_t> execs(n, nullptr);
         std::vector<int> number(n, 1);
         const size_t tb = 2 * n;  // timing events start here
         for (size_t j = 0; j < n; ++j) {
-            if (out[j].status != TUNER_S_OK) continue;
+            if (out[j].status != TUNER_S_OK || cut[j]) continue;
             ctx.split = split[j];
             int num = t->opts.number;
             if (num <= 0) {
@@ -226,6 +236,10 @@ struct GpuMeasurer : Measurer {
         for (size_t j = 0; j < n; ++j) {
             if (out[j].status != TUNER_S_OK) {
                 out[j].cost_ns = INFINITY;
+                continue;
+            }
+            if (cut[j]) {
+                out[j].cost_ns = tver[j];
                 continue;
             }
             const size_t b = tb + j * (size_t)(R + 1);

@@ -95,7 +95,8 @@ tuner_status nccl_unique_id(void* out128);
 struct Measurer {
     virtual ~Measurer() = default;
     // measure `pts` (this rank's share of a batch) -> results in the same order
-    virtual tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out) = 0;
+    // `incumbent` = best cost measured so far (for the early cut)
+    virtual tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out, double incumbent) = 0;
     virtual bool valid(const Pt& p) = 0;
 };
 
@@ -123,6 +124,7 @@ struct Tuner {
     std::unique_ptr<Measurer> measurer;
     std::unique_ptr<Comm> comm;
     tuner_stats stats{};
+    double best_cost = INFINITY;
 
     uint64_t linear(const Pt& p) const;
     Pt from_public(const tuner_point& tp, tuner_status& st) const;  // validates dims/ranges

@@ -107,7 +107,7 @@ tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
     }
     std::vector<Result> lres;
     const int64_t launches0 = g_launch_counter_ptr()->load();
-    tuner_status st = measurer->measure(local, lres);
+    tuner_status st = measurer->measure(local, lres, best_cost);
     stats.kernel_launches += g_launch_counter_ptr()->load() - launches0;
     if (st != TUNER_OK) return st;
     for (auto& x : lres) x.rank = r;
@@ -145,6 +145,7 @@ tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
         smp.rank = res[j].rank;
         memo[linear(batch[j])] = history.size();
         history.push_back(smp);
+        if (smp.cost_ns < best_cost) best_cost = smp.cost_ns;
     }
     stats.candidates += (int64_t)batch.size();
     stats.batches++;
@@ -277,7 +278,7 @@ struct TableMeasurer : Measurer {
     Tuner* t;
     std::vector<double> table;
     TableMeasurer(Tuner* tt, std::vector<double>&& tab) : t(tt), table(std::move(tab)) {}
-    tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out) override {
+    tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out, double) override {
         out.resize(pts.size());
         for (size_t i = 0; i < pts.size(); ++i) {
             out[i] = Result{table[t->linear(pts[i])], 0.0, TUNER_S_OK, 0};
@@ -349,6 +350,7 @@ extern "C" tuner_status tuner_create(int32_t op, const tuner_shape* shape, const
     t->op = op;
     t->shape = *shape;
     t->opts = *opts;
+    if (!(t->opts.early_cut >= 0.0)) return fail(TUNER_EINVAL, "early_cut must be >= 0");
     if (t->opts.repeats < 1 || t->opts.warmup < 0 || t->opts.number < 0 || t->opts.max_batch < 1)
         return fail(TUNER_EINVAL, "repeats >= 1, warmup >= 0, number >= 0, max_batch >= 1 required");
     if (t->opts.alpha != 0.0) return fail(TUNER_EINVAL, "only alpha = 0 (strict median compare) is supported");

@@ -114,7 +114,7 @@ class Tuner:
                  seed: int = 0, policy: str = "grow", cost_table=None,
                  x=None, w=None, y=None, y_ref=None, y_absref=None, stream=None, group=None,
                  warmup: int = 2, repeats: int = 10, number: int = 0, max_batch: int = 512,
-                 verify: bool = True, timeout_ms: float = 1000.0):
+                 verify: bool = True, timeout_ms: float = 1000.0, early_cut: float = 0.0):
         lib = L.lib()
         self._h = C.c_void_p()
         self.op = op
@@ -135,7 +135,7 @@ class Tuner:
         lib.tuner_opts_default(C.byref(o))
         o.warmup, o.repeats, o.number = warmup, repeats, number
         o.timeout_ms, o.seed, o.policy = timeout_ms, seed, L.POLICY[policy]
-        o.max_batch, o.verify = max_batch, int(bool(verify))
+        o.max_batch, o.verify, o.early_cut = max_batch, int(bool(verify)), float(early_cut)
         if cost_table is not None:
             import numpy as np
             tab = np.ascontiguousarray(cost_table, dtype=np.float64)
