@@ -24,7 +24,7 @@ static std::vector<SketchDesc> build_catalogue() {
     // BK staged by TMA with 128-byte swizzle, STAGES-deep mbarrier pipeline,
     // split-K (runtime).
     const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K"};
-    const std::vector<std::vector<int32_t>> tc_vals = {{128}, {64, 128, 256}, {64}, {2, 3, 4, 6}, {1, 2, 4}};
+    const std::vector<std::vector<int32_t>> tc_vals = {{128}, {64, 128, 256}, {64, 128}, {2, 3, 4, 6}, {1, 2, 4}};
     c.push_back({SK_TC_GEMM_BF16, "tc_gemm_bf16", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL), TUNER_BF16,
                  tc_names, tc_vals});
     c.push_back({SK_TC_IGEMM_CONV_BF16, "tc_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tc_names, tc_vals});

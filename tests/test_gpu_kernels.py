@@ -181,3 +181,53 @@ def test_config1_bruteforce_and_droplet():
                     q = list(rep["best"][1]); q[d] = i; sp_ring.append((0, tuple(q)))
         assert all(cost[q] >= rep["best_cost"] for q in sp_ring)
     print(f"config1: droplet {rep['best_cost']:.0f} ns in {rep['trials_used']} trials; brute force {best_bf:.0f} ns")
+
+
+# ---------------------------------------------------------------- tcgen05 bf16 sketch
+def bf16_case(b, m, n, k, dist, seed):
+    x, w = tensors([(b, m, k), (b, n, k)], seed, dist)
+    x, w = on.round_bf16(x), on.round_bf16(w)  # RNE before both paths (R-C4)
+    yo, ao = oc.bmm(x, w)
+    xd = torch.from_numpy(x).to(dev()).to(torch.bfloat16)
+    wd = torch.from_numpy(w).to(dev()).to(torch.bfloat16)
+    return xd, wd, yo, ao
+
+
+@pytest.mark.parametrize("shape", [(1, 200, 136, 72), (2, 128, 256, 256), (1, 512, 384, 1024), (3, 77, 300, 40)])
+def test_tc_gemm_all_configs_vs_oracle(shape):
+    b, m, n, k = shape
+    op = "dense" if b == 1 else "batch_matmul"
+    xd, wd, yo, ao = bf16_case(b, m, n, k, "uniform", sum(shape))
+    y = torch.empty(b, m, n, device=dev())
+    t = Tuner(op, {"b": b, "m": m, "n": n, "k": k}, dtype="bf16", spaces=[(2, sketch_space(2))], x=xd, w=wd, y=y)
+    pts = [p for p in all_points(2) if t.valid(p)]
+    assert len(pts) >= 10
+    bad, worst = [], 0.0
+    for p, yv in run_points(t, pts, xd, wd, y):
+        e = on.max_rel_err(yv.reshape(yo.shape), yo, ao)
+        worst = max(worst, e)
+        if not e <= 1e-5:  # fp32 accumulation of exact bf16 products: far inside the 2e-2 bar
+            bad.append((t.values(p), e))
+    assert not bad, bad[:5]
+    print("tc_gemm worst err", worst)
+
+
+def test_tc_gemm_exact_integer_inputs():
+    b, m, n, k = 1, 256, 192, 320
+    xd, wd, yo, _ = bf16_case(b, m, n, k, "int", 7)
+    y = torch.empty(b, m, n, device=dev())
+    t = Tuner("dense", {"m": m, "n": n, "k": k}, dtype="bf16", spaces=[(2, sketch_space(2))], x=xd, w=wd, y=y)
+    pts = [p for p in all_points(2) if t.valid(p)]
+    for p, yv in run_points(t, pts, xd, wd, y):
+        np.testing.assert_array_equal(yv.reshape(yo.shape), yo.astype(np.float32), err_msg=str(t.values(p)))
+
+
+def test_tc_harness_bert_like():
+    m, n, k = 1024, 768, 768
+    xd, wd, yo, ao = bf16_case(1, m, n, k, "uniform", 12)
+    y = torch.empty(m, n, device=dev())
+    t = Tuner("dense", {"m": m, "n": n, "k": k}, dtype="bf16", x=xd, w=wd, y=y, seed=1)
+    smp = t.sample(40)
+    assert smp and all(s.status == "ok" and s.max_err <= 2e-2 for s in smp), smp[:3]
+    rep = t.droplet(t.best().point, 50)
+    print("tc best", t.values(rep["best"]), rep["best_cost"], "ns", 2 * m * n * k / rep["best_cost"] / 1e3, "TF")
