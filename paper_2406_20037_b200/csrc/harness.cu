@@ -39,18 +39,24 @@ static tuner_status cuda_fail(cudaError_t e, const char* what) {
     } while (0)
 
 // launcher + runtime knobs of a point
-static LaunchFn resolve(const Tuner* t, const Pt& p, int& split) {
+struct RuntimeKnobs {
+    int split = 1, vec = 1, stages = 1;
+};
+static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
     int32_t v[TUNER_MAX_KNOBS];
     t->values_of(p, v);
     const int32_t sk = t->spaces[p.pos].sketch;
+    rk = RuntimeKnobs{};
     switch (sk) {
         case SK_SIMT_GEMM_F32:
         case SK_SIMT_IGEMM_CONV_F32:
-            split = v[5];
+            rk.vec = v[5];
+            rk.stages = v[6];
+            rk.split = v[7];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[4]));
         case SK_TC_GEMM_BF16:
         case SK_TC_IGEMM_CONV_BF16:
-            split = v[4];
+            rk.split = v[4];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], 0));
         default: return nullptr;
     }
@@ -121,8 +127,8 @@ struct GpuMeasurer : Measurer {
         int32_t v[TUNER_MAX_KNOBS];
         t->values_of(p, v);
         if (!sketch_valid(t->spaces[p.pos].sketch, t->info, v)) return false;
-        int split = 1;
-        return resolve(t, p, split) != nullptr;
+        RuntimeKnobs rk;
+        return resolve(t, p, rk) != nullptr;
     }
 
     tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out, double incumbent) override {
@@ -142,16 +148,21 @@ struct GpuMeasurer : Measurer {
             err_cap = n;
         }
         std::vector<LaunchFn> fn(n);
-        std::vector<int> split(n, 1);
+        std::vector<RuntimeKnobs> rk(n);
         std::vector<char> launched(n, 0);
-        for (size_t j = 0; j < n; ++j) fn[j] = resolve(t, pts[j], split[j]);
+        for (size_t j = 0; j < n; ++j) fn[j] = resolve(t, pts[j], rk[j]);
         const size_t ybytes = (size_t)t->info.y_elems * sizeof(float);
-        LaunchCtx ctx{&t->info, t->opts.x, t->opts.w, t->opts.y, 1, st, nsm};
+        LaunchCtx ctx{&t->info, t->opts.x, t->opts.w, t->opts.y, 1, 1, 1, st, nsm};
+        auto set_knobs = [&](size_t j) {
+            ctx.split = rk[j].split;
+            ctx.vec = rk[j].vec;
+            ctx.stages = rk[j].stages;
+        };
 
         // ---- phase 1: verification run (also the first, untimed-for-cost launch)
         CU(cudaMemsetAsync(d_err, 0, n * sizeof(unsigned), st));
         for (size_t j = 0; j < n; ++j) {
-            ctx.split = split[j];
+            set_knobs(j);
             if (t->opts.verify) CU(cudaMemsetAsync(t->opts.y, 0xFF, ybytes, st));
             CU(cudaEventRecord(ev[2 * j], st));
             cudaError_t e = fn[j] ? fn[j](ctx) : cudaErrorInvalidDeviceFunction;
@@ -196,7 +207,7 @@ struct GpuMeasurer : Measurer {
         const size_t tb = 2 * n;  // timing events start here
         for (size_t j = 0; j < n; ++j) {
             if (out[j].status != TUNER_S_OK || cut[j]) continue;
-            ctx.split = split[j];
+            set_knobs(j);
             int num = t->opts.number;
             if (num <= 0) {
                 double want = 20000.0 / std::max(tver[j], 1.0);
@@ -266,13 +277,13 @@ tuner_status make_gpu_measurer(Tuner* t, std::unique_ptr<Measurer>& out) {
 }
 
 tuner_status gpu_kernel_run(const Tuner* t, const Pt& p, const tuner_buffers* buf, void* stream) {
-    int split = 1;
-    LaunchFn fn = resolve(t, p, split);
+    RuntimeKnobs rk;
+    LaunchFn fn = resolve(t, p, rk);
     if (!fn) return fail(TUNER_ERANGE, "schedule not compiled");
     int nsm = 148, dev = 0;
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    LaunchCtx ctx{&t->info, buf->x, buf->w, buf->y, split, (cudaStream_t)stream, nsm};
+    LaunchCtx ctx{&t->info, buf->x, buf->w, buf->y, rk.split, rk.vec, rk.stages, (cudaStream_t)stream, nsm};
     CU(fn(ctx));
     return TUNER_OK;
 }

@@ -15,6 +15,8 @@ struct LaunchCtx {
     const void* w;
     void* y;
     int split;             // runtime SPLIT_K knob
+    int vec;               // runtime VEC knob (SIMT)
+    int stages;            // runtime STAGES knob (SIMT)
     cudaStream_t stream;
     int num_sms;
 };

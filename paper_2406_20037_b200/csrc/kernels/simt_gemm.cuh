@@ -3,18 +3,19 @@
 // One fixed sequence of transformations (a "sketch", Def. 2.1) of
 // the naive loop nest Y[m,n] = sum_k A[m,k] B[n,k]: split m and n into BM x BN
 // block tiles bound to CTAs, split each block tile into TT x TT register tiles
-// bound to threads, split k into BK-wide steps staged through shared memory
-// (double-buffered through registers so the next tile's global loads overlap
-// this tile's FMAs), unroll the inner k loop by UNROLL, and optionally split
-// the k range across SPLIT_K CTAs whose partial sums are reduced with vector
-// atomics.  The annotations (BM, BN, BK, TT, UNROLL, SPLIT_K) are the knobs.
+// bound to threads, split k into BK-wide steps staged through shared memory,
+// unroll the inner k loop by UNROLL, and optionally split the k range across
+// SPLIT_K CTAs whose partial sums are reduced with vector atomics.
+// Annotations (the knobs): BM, BN, BK, TT, UNROLL (compile-time), VEC (global
+// load width: 1 = scalar, 4 = 128-bit), STAGES (shared-memory staging depth:
+// 1 = load/sync/compute, 2 = the next tile's global loads are issued into
+// registers before this tile's FMAs), SPLIT_K (runtime).
 //
 // CONV = true is the implicit-GEMM view of conv2d (NHWC x KRSC -> NPQK):
 // A[m, kk] = X[n, p*sh-ph+r*dh, q*sw-pw+s*dw, c] with m = (n,p,q), kk = (r,s,c),
 // gathered on the fly (zero outside the image); B = W viewed as [K][R*S*C].
 //
-// FP32 on the CUDA cores (north_star: "The fp32 SIMT variants stay on CUDA
-// cores"); 128-bit global loads whenever the reduction run allows (VEC4).
+// FP32 on the CUDA cores (north_star: "The fp32 SIMT variants stay on CUDA cores").
 #pragma once
 #include "common.cuh"
 
@@ -29,8 +30,11 @@ struct SimtParams {
     int ktiles, kt_per_split, split;
     // implicit GEMM (conv) geometry
     int H, W, Cin, P, Q, S, sh, sw, ph, pw, dh, dw;
-    int vec4;
+    int vec4;    // VEC knob == 4
+    int stages;  // STAGES knob
 };
+
+constexpr int cdiv_c(int a, int b) { return (a + b - 1) / b; }
 
 template <int BM, int BN, int BK, int TT>
 struct SimtCfg {
@@ -38,22 +42,16 @@ struct SimtCfg {
     static constexpr int TX = BN / TT;
     static constexpr int LDA = BM + 4;
     static constexpr int LDB = BN + 4;
-    static constexpr int SA1 = (BM * BK + NT - 1) / NT;      // scalar staging per thread
-    static constexpr int SB1 = (BN * BK + NT - 1) / NT;
-    static constexpr int SA4 = (BM * BK / 4 + NT - 1) / NT;  // float4 staging per thread
-    static constexpr int SB4 = (BN * BK / 4 + NT - 1) / NT;
-    static constexpr int STAGE_FLOATS = (SA1 > 4 * SA4 ? SA1 : 4 * SA4) + (SB1 > 4 * SB4 ? SB1 : 4 * SB4);
+    static constexpr int KV = BK / 4;                    // 4-element k groups per row
+    static constexpr int SA = cdiv_c(BM * KV, NT);       // float4 staging slots per thread (A)
+    static constexpr int SB = cdiv_c(BN * KV, NT);       // (B)
     static constexpr size_t SMEM = (size_t)2 * BK * (LDA + LDB) * sizeof(float) + 3 * BM * sizeof(int);
 };
 
 // compile-time half of the static validity rule (the runtime half is in sketches.cpp)
-constexpr int cdiv_c(int a, int b) { return (a + b - 1) / b; }
-constexpr int simt_stage(int BMN, int BK, int NT) {
-    return cdiv_c(BMN * BK, NT) > 4 * cdiv_c(BMN * BK / 4, NT) ? cdiv_c(BMN * BK, NT) : 4 * cdiv_c(BMN * BK / 4, NT);
-}
 constexpr bool simt_static_ok(int BM, int BN, int BK, int TT) {
     return TT <= BM && TT <= BN && (BM / TT) * (BN / TT) <= 1024 &&
-           simt_stage(BM, BK, (BM / TT) * (BN / TT)) + simt_stage(BN, BK, (BM / TT) * (BN / TT)) <= 64;
+           4 * (cdiv_c(BM * (BK / 4), (BM / TT) * (BN / TT)) + cdiv_c(BN * (BK / 4), (BM / TT) * (BN / TT))) <= 64;
 }
 
 // Row r of a thread's TT-row register tile -> row inside the block tile.
@@ -81,7 +79,7 @@ template <int BM, int BN, int BK, int TT, int UNROLL, bool CONV>
 __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
     simt_gemm_f32_kernel(const SimtParams p) {
     using Cfg = SimtCfg<BM, BN, BK, TT>;
-    constexpr int NT = Cfg::NT, TX = Cfg::TX, LDA = Cfg::LDA, LDB = Cfg::LDB;
+    constexpr int NT = Cfg::NT, TX = Cfg::TX, LDA = Cfg::LDA, LDB = Cfg::LDB, KV = Cfg::KV;
     extern __shared__ __align__(16) float smem[];
     float* As = smem;                              // [2][BK][LDA]
     float* Bs = smem + 2 * BK * LDA;               // [2][BK][LDB]
@@ -127,34 +125,19 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
 #pragma unroll
         for (int j = 0; j < TT; ++j) acc[i][j] = 0.f;
 
-    // staging registers: large enough for either load path
-    constexpr int SA = Cfg::SA1 > 4 * Cfg::SA4 ? Cfg::SA1 : 4 * Cfg::SA4;
-    constexpr int SB = Cfg::SB1 > 4 * Cfg::SB4 ? Cfg::SB1 : 4 * Cfg::SB4;
-    float ra[SA], rb[SB];
+    // staging registers: each slot holds 4 consecutive k of one row
+    float4 ra[Cfg::SA], rb[Cfg::SB];
 
-    // A element loader (dense or implicit GEMM)
-    auto load_a1 = [&](int row, int kk, RSC rsc) -> float {
-        const int m = m0 + row;
-        if (m >= p.M || kk >= p.K) return 0.f;
+    // one A element (dense or implicit GEMM), zero outside the problem
+    auto a_elem = [&](int row, int kk, RSC rsc) -> float {
+        if (kk >= p.K) return 0.f;
         if constexpr (CONV) {
             const int h = rowinfo[BM + row] + rsc.r * p.dh;
             const int w = rowinfo[2 * BM + row] + rsc.s * p.dw;
             if ((unsigned)h >= (unsigned)p.H || (unsigned)w >= (unsigned)p.W) return 0.f;
             return __ldg(A + rowinfo[row] + (h * p.W + w) * p.Cin + rsc.c);
         } else {
-            return __ldg(A + (long long)m * p.K + kk);
-        }
-    };
-    auto load_a4 = [&](int row, int kk, RSC rsc) -> float4 {
-        const int m = m0 + row;
-        if (m >= p.M || kk >= p.K) return make_float4(0.f, 0.f, 0.f, 0.f);
-        if constexpr (CONV) {
-            const int h = rowinfo[BM + row] + rsc.r * p.dh;
-            const int w = rowinfo[2 * BM + row] + rsc.s * p.dw;
-            if ((unsigned)h >= (unsigned)p.H || (unsigned)w >= (unsigned)p.W) return make_float4(0.f, 0.f, 0.f, 0.f);
-            return __ldg(reinterpret_cast<const float4*>(A + rowinfo[row] + (h * p.W + w) * p.Cin + rsc.c));
-        } else {
-            return __ldg(reinterpret_cast<const float4*>(A + (long long)m * p.K + kk));
+            return __ldg(A + (long long)(m0 + row) * p.K + kk);
         }
     };
 
@@ -167,96 +150,86 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
             base.s = rs % p.S;
             base.r = rs / p.S;
         }
-        if (p.vec4) {
-            constexpr int KV = BK / 4;
 #pragma unroll
-            for (int i = 0; i < Cfg::SA4; ++i) {
-                const int e = tid + i * NT;
-                const int row = e / KV, kl = (e % KV) * 4;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (e < BM * KV) {
-                    RSC rsc = base;
-                    if constexpr (CONV) rsc = rsc_advance(base, kl, p.Cin, p.S);
-                    v = load_a4(row, k0 + kl, rsc);
+        for (int i = 0; i < Cfg::SA; ++i) {
+            const int e = tid + i * NT;
+            const int row = e / KV, kl = (e % KV) * 4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (e < BM * KV && m0 + row < p.M) {
+                RSC rsc = base;
+                if constexpr (CONV) rsc = rsc_advance(base, kl, p.Cin, p.S);
+                const int kk = k0 + kl;
+                if (p.vec4) {  // VEC = 4: one 128-bit load (K or C is a multiple of 4)
+                    if (kk < p.K) {
+                        if constexpr (CONV) {
+                            const int h = rowinfo[BM + row] + rsc.r * p.dh;
+                            const int w = rowinfo[2 * BM + row] + rsc.s * p.dw;
+                            if ((unsigned)h < (unsigned)p.H && (unsigned)w < (unsigned)p.W)
+                                v = __ldg(reinterpret_cast<const float4*>(A + rowinfo[row] + (h * p.W + w) * p.Cin +
+                                                                          rsc.c));
+                        } else {
+                            v = __ldg(reinterpret_cast<const float4*>(A + (long long)(m0 + row) * p.K + kk));
+                        }
+                    }
+                } else {  // VEC = 1: four scalar loads
+                    v.x = a_elem(row, kk, rsc);
+                    if constexpr (CONV) rsc = rsc_advance(rsc, 1, p.Cin, p.S);
+                    v.y = a_elem(row, kk + 1, rsc);
+                    if constexpr (CONV) rsc = rsc_advance(rsc, 1, p.Cin, p.S);
+                    v.z = a_elem(row, kk + 2, rsc);
+                    if constexpr (CONV) rsc = rsc_advance(rsc, 1, p.Cin, p.S);
+                    v.w = a_elem(row, kk + 3, rsc);
                 }
-                ra[4 * i + 0] = v.x; ra[4 * i + 1] = v.y; ra[4 * i + 2] = v.z; ra[4 * i + 3] = v.w;
             }
+            ra[i] = v;
+        }
 #pragma unroll
-            for (int i = 0; i < Cfg::SB4; ++i) {
-                const int e = tid + i * NT;
-                const int row = e / KV, kl = (e % KV) * 4;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (e < BN * KV && n0 + row < p.N && k0 + kl < p.K)
-                    v = __ldg(reinterpret_cast<const float4*>(B + (long long)(n0 + row) * p.K + k0 + kl));
-                rb[4 * i + 0] = v.x; rb[4 * i + 1] = v.y; rb[4 * i + 2] = v.z; rb[4 * i + 3] = v.w;
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < Cfg::SA1; ++i) {
-                const int e = tid + i * NT;
-                const int row = e / BK, kl = e % BK;
-                float v = 0.f;
-                if (e < BM * BK) {
-                    RSC rsc = base;
-                    if constexpr (CONV) rsc = rsc_advance(base, kl, p.Cin, p.S);
-                    v = load_a1(row, k0 + kl, rsc);
+        for (int i = 0; i < Cfg::SB; ++i) {
+            const int e = tid + i * NT;
+            const int row = e / KV, kl = (e % KV) * 4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int kk = k0 + kl;
+            if (e < BN * KV && n0 + row < p.N) {
+                const float* bp = B + (long long)(n0 + row) * p.K + kk;
+                if (p.vec4) {
+                    if (kk < p.K) v = __ldg(reinterpret_cast<const float4*>(bp));
+                } else {
+                    if (kk < p.K) v.x = __ldg(bp);
+                    if (kk + 1 < p.K) v.y = __ldg(bp + 1);
+                    if (kk + 2 < p.K) v.z = __ldg(bp + 2);
+                    if (kk + 3 < p.K) v.w = __ldg(bp + 3);
                 }
-                ra[i] = v;
             }
-#pragma unroll
-            for (int i = 0; i < Cfg::SB1; ++i) {
-                const int e = tid + i * NT;
-                const int row = e / BK, kl = e % BK;
-                float v = 0.f;
-                if (e < BN * BK && n0 + row < p.N && k0 + kl < p.K) v = __ldg(B + (long long)(n0 + row) * p.K + k0 + kl);
-                rb[i] = v;
-            }
+            rb[i] = v;
         }
     };
     auto sstore = [&](int buf) {
         float* as = As + buf * BK * LDA;
         float* bs = Bs + buf * BK * LDB;
-        if (p.vec4) {
-            constexpr int KV = BK / 4;
 #pragma unroll
-            for (int i = 0; i < Cfg::SA4; ++i) {
-                const int e = tid + i * NT;
-                if (e < BM * KV) {
-                    const int row = e / KV, kl = (e % KV) * 4;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) as[(kl + j) * LDA + row] = ra[4 * i + j];
-                }
+        for (int i = 0; i < Cfg::SA; ++i) {
+            const int e = tid + i * NT;
+            if (e < BM * KV) {
+                const int row = e / KV, kl = (e % KV) * 4;
+                as[(kl + 0) * LDA + row] = ra[i].x;
+                as[(kl + 1) * LDA + row] = ra[i].y;
+                as[(kl + 2) * LDA + row] = ra[i].z;
+                as[(kl + 3) * LDA + row] = ra[i].w;
             }
+        }
 #pragma unroll
-            for (int i = 0; i < Cfg::SB4; ++i) {
-                const int e = tid + i * NT;
-                if (e < BN * KV) {
-                    const int row = e / KV, kl = (e % KV) * 4;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) bs[(kl + j) * LDB + row] = rb[4 * i + j];
-                }
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < Cfg::SA1; ++i) {
-                const int e = tid + i * NT;
-                if (e < BM * BK) as[(e % BK) * LDA + e / BK] = ra[i];
-            }
-#pragma unroll
-            for (int i = 0; i < Cfg::SB1; ++i) {
-                const int e = tid + i * NT;
-                if (e < BN * BK) bs[(e % BK) * LDB + e / BK] = rb[i];
+        for (int i = 0; i < Cfg::SB; ++i) {
+            const int e = tid + i * NT;
+            if (e < BN * KV) {
+                const int row = e / KV, kl = (e % KV) * 4;
+                bs[(kl + 0) * LDB + row] = rb[i].x;
+                bs[(kl + 1) * LDB + row] = rb[i].y;
+                bs[(kl + 2) * LDB + row] = rb[i].z;
+                bs[(kl + 3) * LDB + row] = rb[i].w;
             }
         }
     };
-
-    gload(kt_begin);
-    sstore(0);
-    __syncthreads();
-    int buf = 0;
-    for (int kt = kt_begin; kt < kt_end; ++kt) {
-        const bool more = kt + 1 < kt_end;
-        if (more) gload(kt + 1);  // global loads in flight during the FMAs below
+    auto compute = [&](int buf) {
         const float* as = As + buf * BK * LDA;
         const float* bs = Bs + buf * BK * LDB;
 #pragma unroll UNROLL
@@ -280,10 +253,30 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
 #pragma unroll
                 for (int j = 0; j < TT; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
         }
-        if (more) {
-            sstore(buf ^ 1);
+    };
+
+    if (p.stages >= 2) {  // STAGES = 2: register prefetch of the next tile overlaps the FMAs
+        gload(kt_begin);
+        sstore(0);
+        __syncthreads();
+        int buf = 0;
+        for (int kt = kt_begin; kt < kt_end; ++kt) {
+            const bool more = kt + 1 < kt_end;
+            if (more) gload(kt + 1);
+            compute(buf);
+            if (more) {
+                sstore(buf ^ 1);
+                __syncthreads();
+                buf ^= 1;
+            }
+        }
+    } else {  // STAGES = 1: load, sync, compute, sync
+        for (int kt = kt_begin; kt < kt_end; ++kt) {
+            gload(kt);
+            sstore(0);
             __syncthreads();
-            buf ^= 1;
+            compute(0);
+            __syncthreads();
         }
     }
 
@@ -341,7 +334,8 @@ cudaError_t simt_launch(const LaunchCtx& c) {
     p.kt_per_split = (p.ktiles + c.split - 1) / c.split;
     p.H = (int)s.h; p.W = (int)s.w; p.Cin = (int)s.c; p.P = (int)s.p; p.Q = (int)s.q; p.S = (int)s.s;
     p.sh = s.sh; p.sw = s.sw; p.ph = s.ph; p.pw = s.pw; p.dh = s.dh; p.dw = s.dw;
-    p.vec4 = (BK % 4 == 0) && (CONV ? (s.c % 4 == 0) : (s.K % 4 == 0));
+    p.vec4 = c.vec == 4;
+    p.stages = c.stages;
     if (c.split > 1) {
         cudaError_t e = cudaMemsetAsync(c.y, 0, (size_t)s.y_elems * sizeof(float), c.stream);
         if (e != cudaSuccess) return e;

@@ -2,6 +2,8 @@
 #pragma once
 #include <cstdint>
 
+#include "../../include/tuner.h"
+
 namespace db200 {
 
 enum SketchId : int32_t {

@@ -13,9 +13,10 @@ static std::vector<SketchDesc> build_catalogue() {
     // SIMT fp32 GEMM family: block tile BM x BN, K step BK, TT x TT register tile
     // per thread, inner-k UNROLL, split-K (runtime; partial sums reduced with
     // vector atomics into a zeroed Y).
-    const std::vector<const char*> simt_names = {"BM", "BN", "BK", "TT", "UNROLL", "SPLIT_K"};
-    const std::vector<std::vector<int32_t>> simt_vals = {
-        {16, 32, 64, 128}, {16, 32, 64, 128}, {4, 8, 16, 32}, {2, 4, 8}, {1, 2, 4, 8}, {1, 2, 4, 8, 16}};
+    const std::vector<const char*> simt_names = {"BM", "BN", "BK", "TT", "UNROLL", "VEC", "STAGES", "SPLIT_K"};
+    const std::vector<std::vector<int32_t>> simt_vals = {{16, 32, 64, 128}, {16, 32, 64, 128}, {4, 8, 16, 32},
+                                                         {2, 4, 8},         {1, 2, 4, 8},       {1, 4},
+                                                         {1, 2},            {1, 2, 4, 8, 16}};
     c.push_back({SK_SIMT_GEMM_F32, "simt_gemm_f32", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL),
                  TUNER_F32, simt_names, simt_vals});
     c.push_back({SK_SIMT_IGEMM_CONV_F32, "simt_igemm_conv_f32", 1 << TUNER_OP_CONV2D, TUNER_F32, simt_names,
@@ -79,24 +80,17 @@ bool make_shape_info(int32_t op, const tuner_shape& s, ShapeInfo& o, std::string
     return true;
 }
 
-// SIMT: vector width the kernel will use for global loads (128-bit when the
-// reduction run allows it, R-K2).
-int simt_vec(const ShapeInfo& sh, int bk) {
-    if (bk % 4) return 1;
-    if (sh.op == TUNER_OP_CONV2D) return (sh.c % 4 == 0) ? 4 : 1;
-    return (sh.K % 4 == 0) ? 4 : 1;
-}
-
 static bool simt_valid(const ShapeInfo& sh, const int32_t* v) {
-    const int bm = v[0], bn = v[1], bk = v[2], tt = v[3], split = v[5];
+    const int bm = v[0], bn = v[1], bk = v[2], tt = v[3], vec = v[5], split = v[7];
     if (sh.dtype != TUNER_F32) return false;
     if (tt > bm || tt > bn) return false;
     const int threads = (bm / tt) * (bn / tt);
     if (threads > 1024 || threads < 1) return false;
-    const int vec = simt_vec(sh, bk);
-    const int la = (bm * bk / vec + threads - 1) / threads;  // A vectors staged per thread
-    const int lb = (bn * bk / vec + threads - 1) / threads;
-    if ((la + lb) * vec > 64) return false;  // register budget for the staging buffers
+    const int la = (bm * (bk / 4) + threads - 1) / threads;  // float4 staging slots per thread
+    const int lb = (bn * (bk / 4) + threads - 1) / threads;
+    if (4 * (la + lb) > 64) return false;  // register budget for the staging buffers
+    // 128-bit loads need 4 consecutive k inside one row / one (r,s) tap
+    if (vec == 4 && (sh.op == TUNER_OP_CONV2D ? (sh.c % 4) : (sh.K % 4)) != 0) return false;
     const int64_t ktiles = (sh.K + bk - 1) / bk;
     if (split > ktiles) return false;  // empty K slices
     const int64_t ntiles = (sh.N + bn - 1) / bn;

@@ -45,9 +45,10 @@ def test_catalogue():
     assert sketches("conv2d", "f32") == [1]
     assert sketches("dense", "bf16") == [2]
     assert sketch_name(0) == "simt_gemm_f32"
-    assert knob_names(0) == ["BM", "BN", "BK", "TT", "UNROLL", "SPLIT_K"]
+    assert knob_names(0) == ["BM", "BN", "BK", "TT", "UNROLL", "VEC", "STAGES", "SPLIT_K"]
     sp = sketch_space(0)
-    assert sp[0] == [16, 32, 64, 128] and sp[5] == [1, 2, 4, 8, 16]
+    assert sp[0] == [16, 32, 64, 128] and sp[7] == [1, 2, 4, 8, 16]
+    assert knob_names(2) == ["BM", "BN", "BK", "STAGES", "SPLIT_K"]
     assert sketch_name(99) is None
 
 
@@ -56,5 +57,5 @@ def test_measured_mode_rejects_uncompiled_values():
     from paper_2406_20037_b200 import Tuner, TunerError
     x = torch.zeros(4)
     with pytest.raises(TunerError, match="EINVAL"):
-        Tuner("dense", {"m": 4, "n": 4, "k": 4}, spaces=[(0, [[24], [16], [4], [4], [1], [1]])], x=x, w=x, y=x,
+        Tuner("dense", {"m": 4, "n": 4, "k": 4}, spaces=[(0, [[24], [16], [4], [4], [1], [4], [2], [1]])], x=x, w=x, y=x,
               stream=0)

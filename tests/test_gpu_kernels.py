@@ -161,12 +161,12 @@ def test_config1_bruteforce_and_droplet():
     x, w, yo, ao = gemm_case(1, m, n, k, "uniform", 0)
     xd, wd = to_dev(x, w)
     y = torch.empty(m, n, device=dev())
-    space = [[16, 32, 64, 128], [16, 32, 64, 128], [4, 8, 16, 32], [4], [1, 2, 4, 8], [1]]
+    space = [[16, 32, 64, 128], [16, 32, 64, 128], [4, 8, 16, 32], [4], [1, 2, 4, 8], [4], [2], [1]]
     import itertools
     pts = [(0, idx) for idx in itertools.product(*[range(len(v)) for v in space])]
     t = Tuner("dense", {"m": m, "n": n, "k": k}, spaces=[(0, space)], x=xd, w=wd, y=y, policy="grow")
     assert all(t.valid(p) for p in pts) and len(pts) == 256
-    rep = t.droplet((0, (0, 0, 0, 0, 0, 0)), 100)
+    rep = t.droplet((0, (0,) * 8), 100)
     res = t.measure(pts)
     assert all(r.status == "ok" for r in res)
     cost = {r.point: r.cost_ns for r in res}
@@ -174,7 +174,7 @@ def test_config1_bruteforce_and_droplet():
     # converged => local minimum under the paper's neighbourhood (measured costs)
     if rep["converged"]:
         sp_ring = []
-        for d in range(6):
+        for d in range(8):
             for dlt in (-1, 1):
                 i = rep["best"][1][d] + dlt
                 if 0 <= i < len(space[d]):
