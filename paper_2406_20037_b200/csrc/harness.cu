@@ -55,9 +55,11 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
             rk.split = v[7];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[4]));
         case SK_TC_GEMM_BF16:
-        case SK_TC_IGEMM_CONV_BF16:
             rk.split = v[4];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], 0));
+        case SK_TC_IGEMM_CONV_BF16:
+            rk.split = v[4];
+            return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[5]));
         default: return nullptr;
     }
 }

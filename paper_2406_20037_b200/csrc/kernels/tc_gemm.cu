@@ -1,16 +1,25 @@
-// tc_gemm.cu — sketch TC_GEMM_BF16: dense / batch_matmul on the 5th-generation
-// tensor cores.  Y[b,m,n] (fp32) = sum_k X[b,m,k] W[b,n,k], X and W bf16.
+// tc_gemm.cu — sketches TC_GEMM_BF16 and TC_IGEMM_CONV_BF16 on the 5th-generation
+// tensor cores.
+//   dense / bmm : Y[b,m,n] (fp32) = sum_k X[b,m,k] W[b,n,k],  X, W bf16
+//   conv2d      : Y[n,p,q,k] (fp32) = sum_{r,s,c} X[n,p*sh-ph+r*dh,q*sw-pw+s*dw,c] W[k,r,s,c]
 //
-// The sketch (Def. 2.1): tile (m, n) into 128 x BN output tiles, one CTA each
-// (x SPLIT_K slices of the k range); stage BK-wide k slices of A and B through
-// a STAGES-deep shared-memory ring filled by TMA (128-byte swizzle, one
-// mbarrier pair per stage); accumulate in TMEM with tcgen05.mma issued by a
-// single thread (UMMA 128 x BN x 16); drain TMEM with tcgen05.ld in four
-// epilogue warps straight to global memory (fp32), or with vector reductions
-// (red.global.add.v4.f32) into a zeroed Y when SPLIT_K > 1.
+// The sketch (Def. 2.1): tile the output into 128 x BN tiles, one CTA each (x
+// SPLIT_K slices of the reduction); stage BK-wide reduction slices of A and B
+// through a STAGES-deep shared-memory ring filled by TMA (128-byte swizzle, one
+// mbarrier pair per stage); accumulate in TMEM with tcgen05.mma issued by one
+// thread (UMMA 128 x BN x 16, kind::f16, fp32 accumulate); drain TMEM with
+// tcgen05.ld in four epilogue warps straight to global memory, or with vector
+// reductions (red.global.add.v4.f32) into a zeroed Y when SPLIT_K > 1.
+//
+// Implicit GEMM (TQ > 0): a 128-row M tile is a TP x TQ rectangle of output
+// pixels of one image (TP = 128 / TQ).  For filter tap (r, s) and channel block
+// c0 its A slice is ONE 4-D TMA box of X (NHWC) starting at
+// (c0, q0*sw - pw + s*dw, p0*sh - ph + r*dh, n) with traversal strides (sw, sh):
+// the hardware does the im2col gather, the conv stride, and the zero padding
+// (out-of-bounds fill).  B is W (KRSC) as a 4-D box (c0, s, r, k0).
 // Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
 // warps 2..5 = epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).
-// Knobs: BM (128), BN, BK, STAGES, SPLIT_K.
+// Knobs: BM (128), BN, BK, STAGES, SPLIT_K, TILE_Q (conv only).
 #include <cstring>
 
 #include "common.cuh"
@@ -30,18 +39,24 @@ struct TcCfg {
 };
 
 struct TcParams {
-    int M, N, K;
+    int M, N, K;  // GEMM view (conv: M = N*P*Q, N = K_out, K = R*S*C)
     int kblocks, kb_per_split, split;
     float* C;
     long long sC;
+    // implicit GEMM
+    int P, Q, S, CB;  // CB = channel blocks of BK per tap
+    int sh, sw, ph, pw, dh, dw;
+    int tiles_p, tiles_q;
 };
 
-template <int BN, int BK, int STAGES>
+template <int BN, int BK, int STAGES, int TQ>
 __global__ void __launch_bounds__(192, 1)
     tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const TcParams p) {
     using Cfg = TcCfg<BN, BK, STAGES>;
     constexpr int BM = Cfg::BM;
+    constexpr bool CONV = TQ > 0;
+    constexpr int TP = CONV ? BM / TQ : 1;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + STAGES * Cfg::STAGE_BYTES);
@@ -51,12 +66,23 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int n0 = blockIdx.y * BN;
     const int bz = blockIdx.z / p.split, kz = blockIdx.z % p.split;
     const int kb0 = kz * p.kb_per_split;
     const int kb1 = min(p.kblocks, kb0 + p.kb_per_split);
     const int nkb = kb1 - kb0;
     if (nkb <= 0) return;  // uniform per CTA, before any barrier
+    // M tile: rows m0.. (GEMM) or the pixel rectangle (img, p0.., q0..) (conv)
+    int m0 = 0, img = bz, p0 = 0, q0 = 0;
+    if constexpr (CONV) {
+        const int bx = blockIdx.x;
+        q0 = (bx % p.tiles_q) * TQ;
+        const int t = bx / p.tiles_q;
+        p0 = (t % p.tiles_p) * TP;
+        img = t / p.tiles_p;
+    } else {
+        m0 = blockIdx.x * BM;
+    }
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -82,13 +108,28 @@ __global__ void __launch_bounds__(192, 1)
                 tc::mbar_wait(tc::smem_u32(&empty[s]), ph ^ 1u);
                 const uint32_t fb = tc::smem_u32(&full[s]);
                 tc::mbar_expect_tx(fb, Cfg::STAGE_BYTES);
-                const int k0 = (kb0 + i) * BK;
                 const uint32_t sa = tc::smem_u32(base + s * Cfg::STAGE_BYTES);
                 const uint32_t sb = sa + Cfg::A_BYTES;
+                const int kb = kb0 + i;
+                if constexpr (CONV) {
+                    const int cb = kb % p.CB;
+                    const int rs = kb / p.CB;
+                    const int fs = rs % p.S, fr = rs / p.S;
+                    const int wq = q0 * p.sw - p.pw + fs * p.dw;
+                    const int hp = p0 * p.sh - p.ph + fr * p.dh;
 #pragma unroll
-                for (int a = 0; a < BK / 64; ++a) {
-                    tc::tma_load_3d(sa + a * BM * 128, &tmA, fb, k0 + a * 64, m0, bz);
-                    tc::tma_load_3d(sb + a * BN * 128, &tmB, fb, k0 + a * 64, n0, bz);
+                    for (int a = 0; a < BK / 64; ++a) {
+                        const int c0 = cb * BK + a * 64;
+                        tc::tma_load_4d(sa + a * BM * 128, &tmA, fb, c0, wq, hp, img);
+                        tc::tma_load_4d(sb + a * BN * 128, &tmB, fb, c0, fs, fr, n0);
+                    }
+                } else {
+                    const int k0 = kb * BK;
+#pragma unroll
+                    for (int a = 0; a < BK / 64; ++a) {
+                        tc::tma_load_3d(sa + a * BM * 128, &tmA, fb, k0 + a * 64, m0, bz);
+                        tc::tma_load_3d(sb + a * BN * 128, &tmB, fb, k0 + a * 64, n0, bz);
+                    }
                 }
             }
         }
@@ -115,10 +156,20 @@ __global__ void __launch_bounds__(192, 1)
         }
     } else {  // ---- epilogue: TMEM -> registers -> global
         const int q = warp & 3;
-        const int row = m0 + q * 32 + lane;
+        const int trow = q * 32 + lane;  // row of the 128-row tile held by this thread
+        bool row_ok;
+        long long orow;                  // output row index (GEMM row or NPQ pixel)
+        if constexpr (CONV) {
+            const int pp = p0 + trow / TQ, qq = q0 + trow % TQ;
+            row_ok = pp < p.P && qq < p.Q;
+            orow = ((long long)img * p.P + pp) * p.Q + qq;
+        } else {
+            row_ok = m0 + trow < p.M;
+            orow = (long long)bz * p.M + m0 + trow;
+        }
         tc::mbar_wait(tc::smem_u32(tmem_full), 0);
         tc::tc_fence_after();
-        float* crow = p.C + bz * p.sC + (long long)row * p.N;
+        float* crow = p.C + orow * p.N;
         const bool vec_ok = (p.N % 4) == 0;
 #pragma unroll 1
         for (int c = 0; c < BN / 16; ++c) {
@@ -126,7 +177,7 @@ __global__ void __launch_bounds__(192, 1)
             tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 16), r);
             tc::tmem_ld_wait();
             const int n = n0 + c * 16;
-            if (row >= p.M || n >= p.N) continue;
+            if (!row_ok || n >= p.N) continue;
             if (vec_ok && n + 16 <= p.N) {
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
@@ -171,24 +222,30 @@ static EncodeTiledFn encode_tiled() {
     return fn;
 }
 
-// 3-D K-major bf16 operand [batch][rows][K] -> box {64, box_rows, 1}, 128-byte swizzle
-static bool make_kmajor_map(CUtensorMap* m, const void* ptr, int64_t batch, int64_t rows, int64_t K, int box_rows) {
+static bool encode(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                   const cuuint32_t* box, const cuuint32_t* es) {
     EncodeTiledFn enc = encode_tiled();
     if (!enc) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
-    cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)(rows * K * 2)};
-    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int BK, int STAGES>
-cudaError_t tc_gemm_launch(const LaunchCtx& c) {
+// 3-D K-major operand [batch][rows][K] -> box {64, box_rows, 1}
+static bool make_kmajor_map(CUtensorMap* m, const void* ptr, int64_t batch, int64_t rows, int64_t K, int box_rows) {
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)(rows * K * 2)};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return encode(m, ptr, 3, dims, strides, box, es);
+}
+
+template <int BN, int BK, int STAGES, int TQ>
+cudaError_t tc_launch(const LaunchCtx& c) {
     using Cfg = TcCfg<BN, BK, STAGES>;
-    auto kern = tc_gemm_bf16_kernel<BN, BK, STAGES>;
+    constexpr bool CONV = TQ > 0;
+    auto kern = tc_gemm_bf16_kernel<BN, BK, STAGES, TQ>;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -197,21 +254,47 @@ cudaError_t tc_gemm_launch(const LaunchCtx& c) {
     }
     const ShapeInfo& s = *c.sh;
     CUtensorMap ta, tb;
-    if (!make_kmajor_map(&ta, c.x, s.batch, s.M, s.K, Cfg::BM) || !make_kmajor_map(&tb, c.w, s.batch, s.N, s.K, BN))
-        return cudaErrorInvalidValue;
     TcParams p;
+    std::memset(&p, 0, sizeof(p));
     p.M = (int)s.M; p.N = (int)s.N; p.K = (int)s.K;
-    p.kblocks = (int)((s.K + BK - 1) / BK);
     p.split = c.split;
-    p.kb_per_split = (p.kblocks + c.split - 1) / c.split;
     p.C = (float*)c.y;
     p.sC = s.M * s.N;
+    dim3 grid;
+    if constexpr (CONV) {
+        constexpr int TP = 128 / TQ;
+        // X: NHWC as {C, W, H, N}, traversal strides (1, sw, sh, 1); box {64, TQ*sw, TP*sh, 1}
+        cuuint64_t xd[4] = {(cuuint64_t)s.c, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)s.n};
+        cuuint64_t xs[3] = {(cuuint64_t)s.c * 2, (cuuint64_t)(s.w * s.c * 2), (cuuint64_t)(s.h * s.w * s.c * 2)};
+        cuuint32_t xb[4] = {64, (cuuint32_t)(TQ * s.sw), (cuuint32_t)(TP * s.sh), 1};
+        cuuint32_t xe[4] = {1, (cuuint32_t)s.sw, (cuuint32_t)s.sh, 1};
+        // W: KRSC as {C, S, R, K}; box {64, 1, 1, BN}
+        cuuint64_t wd[4] = {(cuuint64_t)s.c, (cuuint64_t)s.s, (cuuint64_t)s.r, (cuuint64_t)s.k};
+        cuuint64_t ws[3] = {(cuuint64_t)s.c * 2, (cuuint64_t)(s.s * s.c * 2), (cuuint64_t)(s.r * s.s * s.c * 2)};
+        cuuint32_t wb[4] = {64, 1, 1, (cuuint32_t)BN};
+        cuuint32_t we[4] = {1, 1, 1, 1};
+        if (!encode(&ta, c.x, 4, xd, xs, xb, xe) || !encode(&tb, c.w, 4, wd, ws, wb, we))
+            return cudaErrorInvalidValue;
+        p.P = (int)s.p; p.Q = (int)s.q; p.S = (int)s.s;
+        p.CB = (int)((s.c + BK - 1) / BK);
+        p.sh = s.sh; p.sw = s.sw; p.ph = s.ph; p.pw = s.pw; p.dh = s.dh; p.dw = s.dw;
+        p.tiles_q = (int)((s.q + TQ - 1) / TQ);
+        p.tiles_p = (int)((s.p + TP - 1) / TP);
+        p.kblocks = (int)(s.r * s.s) * p.CB;
+        grid = dim3((unsigned)(s.n * p.tiles_p * p.tiles_q), (unsigned)((s.N + BN - 1) / BN), (unsigned)c.split);
+    } else {
+        if (!make_kmajor_map(&ta, c.x, s.batch, s.M, s.K, Cfg::BM) ||
+            !make_kmajor_map(&tb, c.w, s.batch, s.N, s.K, BN))
+            return cudaErrorInvalidValue;
+        p.kblocks = (int)((s.K + BK - 1) / BK);
+        grid = dim3((unsigned)((s.M + Cfg::BM - 1) / Cfg::BM), (unsigned)((s.N + BN - 1) / BN),
+                    (unsigned)(s.batch * c.split));
+    }
+    p.kb_per_split = (p.kblocks + c.split - 1) / c.split;
     if (c.split > 1) {
         cudaError_t e = cudaMemsetAsync(c.y, 0, (size_t)s.y_elems * sizeof(float), c.stream);
         if (e != cudaSuccess) return e;
     }
-    dim3 grid((unsigned)((s.M + Cfg::BM - 1) / Cfg::BM), (unsigned)((s.N + BN - 1) / BN),
-              (unsigned)(s.batch * c.split));
     kern<<<grid, Cfg::THREADS, Cfg::SMEM, c.stream>>>(ta, tb, p);
     count_launches(1);
     return cudaGetLastError();
@@ -221,18 +304,25 @@ constexpr bool tc_static_ok(int BN, int BK, int STAGES) {
     return 1024 + (size_t)STAGES * (128 + BN) * BK * 2 + 256 <= 227 * 1024;
 }
 
-template <int BN, int BK, int STAGES>
+template <int BN, int BK, int STAGES, int TQ>
 void tc_register() {
     if constexpr (tc_static_ok(BN, BK, STAGES))
-        registry_add(kernel_key(SK_TC_GEMM_BF16, 128, BN, BK, STAGES, 0), &tc_gemm_launch<BN, BK, STAGES>);
+        registry_add(kernel_key(TQ ? SK_TC_IGEMM_CONV_BF16 : SK_TC_GEMM_BF16, 128, BN, BK, STAGES, TQ),
+                     &tc_launch<BN, BK, STAGES, TQ>);
 }
 
-#define TC_STAGES(BN, BK) \
-    tc_register<BN, BK, 2>(); tc_register<BN, BK, 3>(); tc_register<BN, BK, 4>(); tc_register<BN, BK, 6>();
+#define TC_STAGES(BN, BK, TQ)                                                                         \
+    tc_register<BN, BK, 2, TQ>(); tc_register<BN, BK, 3, TQ>(); tc_register<BN, BK, 4, TQ>(); \
+    tc_register<BN, BK, 6, TQ>();
+#define TC_SHAPES(TQ) \
+    TC_STAGES(64, 64, TQ) TC_STAGES(128, 64, TQ) TC_STAGES(256, 64, TQ) TC_STAGES(64, 128, TQ) \
+    TC_STAGES(128, 128, TQ) TC_STAGES(256, 128, TQ)
 
 void register_tc_gemm() {
-    TC_STAGES(64, 64) TC_STAGES(128, 64) TC_STAGES(256, 64)
-    TC_STAGES(64, 128) TC_STAGES(128, 128) TC_STAGES(256, 128)
+    TC_SHAPES(0)   // dense / bmm
+    TC_SHAPES(8)   // conv, 16 x 8 pixel tiles
+    TC_SHAPES(16)  // conv, 8 x 16
+    TC_SHAPES(32)  // conv, 4 x 32
 }
 
 }  // namespace db200

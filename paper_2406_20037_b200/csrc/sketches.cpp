@@ -28,7 +28,12 @@ static std::vector<SketchDesc> build_catalogue() {
     const std::vector<std::vector<int32_t>> tc_vals = {{128}, {64, 128, 256}, {64, 128}, {2, 3, 4, 6}, {1, 2, 4}};
     c.push_back({SK_TC_GEMM_BF16, "tc_gemm_bf16", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL), TUNER_BF16,
                  tc_names, tc_vals});
-    c.push_back({SK_TC_IGEMM_CONV_BF16, "tc_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tc_names, tc_vals});
+    // implicit-GEMM conv: the 128-row M tile is a (128/TILE_Q) x TILE_Q rectangle of output pixels
+    const std::vector<const char*> tcc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "TILE_Q"};
+    std::vector<std::vector<int32_t>> tcc_vals = tc_vals;
+    tcc_vals.push_back({8, 16, 32});
+    c.push_back({SK_TC_IGEMM_CONV_BF16, "tc_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tcc_names,
+                 tcc_vals});
     return c;
 }
 
@@ -102,15 +107,21 @@ static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
     const int bm = v[0], bn = v[1], bk = v[2], stages = v[3], split = v[4];
     if (sh.dtype != TUNER_BF16) return false;
     // TMA needs 16-byte aligned global strides: K (bf16) multiple of 8.
+    int64_t ktiles;
     if (sh.op == TUNER_OP_CONV2D) {
+        const int tq = v[5], tp = 128 / tq;
         if (sh.c % 8) return false;
-    } else if (sh.K % 8) {
-        return false;
+        if (sh.sh > 8 || sh.sw > 8) return false;                  // TMA traversal stride <= 8
+        if (tq * sh.sw > 256 || tp * sh.sh > 256) return false;    // TMA box extent <= 256
+        if (bk > 64 && sh.c < bk) return false;                    // a fully zero channel block
+        ktiles = sh.r * sh.s * ((sh.c + bk - 1) / bk);
+    } else {
+        if (sh.K % 8) return false;
+        ktiles = (sh.K + bk - 1) / bk;
     }
     const int64_t smem = (int64_t)stages * (bm + bn) * bk * 2 + 1024 /*align*/ + 256 /*barriers*/;
     if (smem > 227 * 1024) return false;
     if (bn > 256 || bm != 128) return false;
-    const int64_t ktiles = (sh.K + bk - 1) / bk;
     if (split > ktiles) return false;
     if ((int64_t)split * sh.batch > 65535) return false;
     return true;
