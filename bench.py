@@ -35,7 +35,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="resnet", choices=["resnet", "resnet18", "resnet50"])
+    ap.add_argument("--workload", default="resnet",
+                    choices=["resnet", "resnet18", "resnet50", "vgg16", "alexnet", "vgg_alexnet", "bert", "bert1",
+                             "config1"])
     ap.add_argument("--n-sample", type=int, default=300)
     ap.add_argument("--droplet-budget", type=int, default=100)
     ap.add_argument("--baseline", type=int, default=10000)
@@ -47,8 +49,12 @@ def parse():
 
 
 def layers_for(name):
-    from synth import RESNET18, RESNET50
-    return {"resnet": RESNET18 + RESNET50, "resnet18": RESNET18, "resnet50": RESNET50}[name]
+    """(layers, dtype) of a BASELINE.json config (configs[1] is the default bench line)."""
+    from synth import ALEXNET, BERT, CONFIG1, RESNET18, RESNET50, VGG16
+    from synth.workloads import bert
+    return {"resnet": (RESNET18 + RESNET50, "f32"), "resnet18": (RESNET18, "f32"), "resnet50": (RESNET50, "f32"),
+            "vgg16": (VGG16, "bf16"), "alexnet": (ALEXNET, "bf16"), "vgg_alexnet": (VGG16 + ALEXNET, "bf16"),
+            "bert": (BERT, "bf16"), "bert1": (bert(batch=1), "bf16"), "config1": ([CONFIG1], "f32")}[name]
 
 
 def peaks():
@@ -61,6 +67,7 @@ def peaks():
     # FP32 FFMA peak from unit counts and clock (B200_PROFILING.md: 148 SMs; 128 FP32 lanes/SM, 2 flop/FFMA)
     fp32_tflops = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
     return {"fp32_tflops": fp32_tflops, "sm_max_mhz": sm_mhz, "hbm_gbs": float(mp.get("hbm_gbs", 6650.0)),
+            "bf16_tflops": float(mp.get("bf16_tflops", 1590.0)),
             "source": "MEASURED_PEAKS.json" if mp else "B200_PROFILING.md fallback"}
 
 
@@ -126,7 +133,10 @@ def oracle_rate(layers, budget_s, seed=0):
     while time.perf_counter() - t0 < budget_s or done == 0:
         L = layers[i % len(layers)]
         x, w = layer_tensors(L, seed + i)
-        oc.conv2d(x, w, L["stride"], L["pad"], L["dil"])
+        if L["op"] == "conv2d":
+            oc.conv2d(x, w, L["stride"], L["pad"], L["dil"])
+        else:
+            oc.bmm(x, w)
         done += 1
         names.append(L["name"])
         i += 1
@@ -138,7 +148,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    layers = layers_for(args.workload)
+    layers, _ = layers_for(args.workload)
     per_step = 5.0
     for i in range(args.warmup):
         oracle_rate([layers[i % len(layers)]], 0.5, seed=i)
@@ -149,11 +159,11 @@ def run_reference(args):
         tot_t += el
         seen += names
     v = tot_c / tot_t
-    sample = f"{tot_c} direct-loop fp64 evaluations of {len(set(seen))} ResNet layers ({tot_t:.1f} s)"
+    sample = f"{tot_c} direct-loop fp64 evaluations of {len(set(seen))} {args.workload} layers ({tot_t:.1f} s)"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "candidates/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "resnet18/50 conv2d b1 224 fp32 (oracle direct loops)"},
+            "config": {"workload": f"{args.workload} layers (oracle direct loops, fp64)"},
             "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -182,29 +192,37 @@ def main():
     from synth import layer_flops, layer_tensors
     from synth.workloads import out_hw
 
-    layers = layers_for(args.workload)
+    layers, dtype = layers_for(args.workload)
     pk = peaks()
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
 
     # CPU baseline: the oracle on this box's host cores, before the GPU work (rank 0, N = 1 only)
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r, n, el, cores, names = oracle_rate(layers[:11], 12.0)
         cpu_baseline = {"value": r, "unit": "candidates/s", "cores": cores, "kind": "oracle",
-                        "sample": f"{n} direct-loop fp64 evaluations over {len(set(names))} ResNet-18 layers "
+                        "sample": f"{n} direct-loop fp64 evaluations over {len(set(names))} {args.workload} layers "
                                   f"({el:.1f} s; one evaluation = one candidate measurement)"}
 
-    # inputs resident in HBM before timing: X, W per layer (seeded U[-1,1))
+    def out_shape(L):
+        if L["op"] == "conv2d":
+            P, Q = out_hw(L)
+            return (L["N"], P, Q, L["K"])
+        return (L.get("b", 1), L["m"], L["n"])
+
+    # inputs resident in HBM before timing: X, W per layer (seeded U[-1,1); bf16 = RNE of it)
     bufs = []
     for i, L in enumerate(layers):
         x, w = layer_tensors(L, 0x5EED + i)
-        P, Q = out_hw(L)
-        bufs.append((torch.from_numpy(x).to(dev), torch.from_numpy(w).to(dev),
-                     torch.empty((L["N"], P, Q, L["K"]), device=dev), x, w))
+        bufs.append((torch.from_numpy(x).to(dev).to(tdt), torch.from_numpy(w).to(dev).to(tdt),
+                     torch.empty(out_shape(L), device=dev), x, w))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
     def shape_of(L):
-        return {k: L[k] for k in ("N", "C", "H", "W", "K", "R", "S", "stride", "pad", "dil")}
+        if L["op"] == "conv2d":
+            return {k: L[k] for k in ("N", "C", "H", "W", "K", "R", "S", "stride", "pad", "dil")}
+        return {k: L[k] for k in ("b", "m", "n", "k") if k in L}
 
     def tune_layer(li, seed, e2e=False, pinned=None):
         L = layers[li]
@@ -215,9 +233,13 @@ def main():
         rec = {"layer": L["name"], "gflop": layer_flops(L) / 1e9}
         # DPAnsor: sample N, best-of-N, Droplet to convergence (<= 100 trials)
         t0 = time.perf_counter()
-        tu = Tuner("conv2d", shape_of(L), x=xd, w=wd, y=y, seed=seed, group=group, stream=stream,
+        tu = Tuner(L["op"], shape_of(L), dtype=dtype, x=xd, w=wd, y=y, seed=seed, group=group, stream=stream,
                    early_cut=args.early_cut)
         smp = tu.sample(args.n_sample)
+        if not smp:  # no compiled sketch covers this layer (e.g. bf16 TMA needs C % 8 == 0)
+            tu.close()
+            rec.update(skipped="no statically valid schedule", candidates=0, launches=0, collectives=0)
+            return rec
         b = tu.best()
         rep = tu.droplet(b.point, args.droplet_budget)
         t1 = time.perf_counter()
@@ -227,7 +249,7 @@ def main():
                    dp_wall_s=t1 - t0, dp_candidates=st["candidates"], launches=st["kernel_launches"],
                    collectives=st["collectives"], wrong=sum(s.status != "ok" for s in tu.history()))
         # the 10,000-trial random baseline on the same harness (fresh history, other seed)
-        bl = Tuner("conv2d", shape_of(L), x=xd, w=wd, y=y, seed=seed + 7919, group=group, stream=stream,
+        bl = Tuner(L["op"], shape_of(L), dtype=dtype, x=xd, w=wd, y=y, seed=seed + 7919, group=group, stream=stream,
                    early_cut=args.early_cut)
         bl.sample(args.baseline) if args.baseline > 0 else None
         t2 = time.perf_counter()
@@ -286,7 +308,8 @@ def main():
     # e2e: host buffers through the public API, H2D + D2H inside the timed region
     e2e = None
     if not args.no_e2e:
-        pinned = [(torch.from_numpy(b[3]).pin_memory(), torch.from_numpy(b[4]).pin_memory()) for b in bufs]
+        pinned = [(torch.from_numpy(b[3]).to(tdt).pin_memory(), torch.from_numpy(b[4]).to(tdt).pin_memory())
+                  for b in bufs]
         barrier()
         t0 = time.perf_counter()
         e_c, h2d, d2h = 0, 0, 0
@@ -294,7 +317,7 @@ def main():
             li = s % len(layers)
             r = tune_layer(li, seed=s, e2e=True, pinned=pinned[li])
             e_c += r["candidates"]
-            h2d += pinned[li][0].numel() * 4 + pinned[li][1].numel() * 4
+            h2d += sum(t.numel() * t.element_size() for t in pinned[li])
             d2h += bufs[li][2].numel() * 4
         barrier()
         el = time.perf_counter() - t0
@@ -306,26 +329,31 @@ def main():
                "d2h_bytes_per_step": d2h // args.steps}
 
     # roofline of the dominant kernel = the best schedule found (FP32 pipe, CUDA-event median per launch)
-    fl = sum(r["gflop"] * 1e9 for r in recs)
-    best_ns = sum(min(r["dp_best_ns"], r["bl_best_ns"]) for r in recs)
-    dp_ns = sum(r["dp_best_ns"] for r in recs)
+    tuned = [r for r in recs if not r.get("skipped")]
+    fl = sum(r["gflop"] * 1e9 for r in tuned)
+    dp_ns = sum(r["dp_best_ns"] for r in tuned)
     achieved = fl / (dp_ns * 1e-9) / 1e12
-    roofline = {"bound": "alu", "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / pk["fp32_tflops"], "traffic": None,
-                "kernel": "best 300+Droplet schedule per layer (simt_igemm_conv_f32), sum F / sum median t",
-                "peak_source": f"148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz (derived)"}
-    dp_wall = sum(r["dp_wall_s"] for r in recs)
-    bl_wall = sum(r["bl_wall_s"] for r in recs)
-    quality = [r["dp_best_ns"] / r["bl_best_ns"] for r in recs if r["bl_best_ns"] < math.inf]
+    if dtype == "f32":
+        peak = pk["fp32_tflops"]
+        roofline = {"bound": "alu", "peak_source": f"148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz "
+                                                   "(derived from B200_PROFILING.md unit counts; no measured FP32 peak)"}
+    else:
+        peak = pk["bf16_tflops"]
+        roofline = {"bound": "tensor", "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst) = {peak}"}
+    roofline.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "kernel": "best 300+Droplet schedule per timed layer; sum F / sum median CUDA-event time"})
+    dp_wall = sum(r["dp_wall_s"] for r in tuned)
+    bl_wall = sum(r["bl_wall_s"] for r in tuned)
+    quality = [r["dp_best_ns"] / r["bl_best_ns"] for r in tuned if r["bl_best_ns"] < math.inf]
     line = {
         "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.workload} conv2d layers b1 224x224 fp32: {args.n_sample} samples + Droplet "
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": {"workload": f"{args.workload} layers ({dtype}): {args.n_sample} samples + Droplet "
                                f"(<= {args.droplet_budget}) vs {args.baseline}-trial random baseline, one layer per step",
                    "layers": [r["layer"] for r in recs], "l2": "flushed between steps; candidate timings hot-L2 "
                    "(back-to-back launches)", "early_cut": args.early_cut, "parallelism": f"candidates sharded x{world}"},
-        "best_schedule_tflops": achieved, "best_schedule_pct_fp32_peak": 100 * achieved / pk["fp32_tflops"],
+        "best_schedule_tflops": achieved, "best_schedule_pct_peak": 100 * achieved / peak,
         "tuning_wall_s": {"dpansor": dp_wall, "baseline_10k": bl_wall,
                           "speedup": bl_wall / dp_wall if dp_wall > 0 else None},
         "quality_dp_over_10k": {"geomean": math.exp(sum(math.log(q) for q in quality) / len(quality)) if quality else None,

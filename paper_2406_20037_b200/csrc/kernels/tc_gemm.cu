@@ -3,13 +3,18 @@
 //   dense / bmm : Y[b,m,n] (fp32) = sum_k X[b,m,k] W[b,n,k],  X, W bf16
 //   conv2d      : Y[n,p,q,k] (fp32) = sum_{r,s,c} X[n,p*sh-ph+r*dh,q*sw-pw+s*dw,c] W[k,r,s,c]
 //
-// The sketch (Def. 2.1): tile the output into 128 x BN tiles, one CTA each (x
-// SPLIT_K slices of the reduction); stage BK-wide reduction slices of A and B
-// through a STAGES-deep shared-memory ring filled by TMA (128-byte swizzle, one
-// mbarrier pair per stage); accumulate in TMEM with tcgen05.mma issued by one
-// thread (UMMA 128 x BN x 16, kind::f16, fp32 accumulate); drain TMEM with
-// tcgen05.ld in four epilogue warps straight to global memory, or with vector
-// reductions (red.global.add.v4.f32) into a zeroed Y when SPLIT_K > 1.
+// The sketch (Def. 2.1): tile the output into 128 x BN tiles (x SPLIT_K slices of
+// the reduction); stage BK-wide reduction slices of A and B through a
+// STAGES-deep shared-memory ring filled by TMA (128-byte swizzle, one mbarrier
+// pair per stage); accumulate in TMEM with tcgen05.mma issued by one thread
+// (UMMA 128 x BN x 16, kind::f16, fp32 accumulate); drain TMEM with tcgen05.ld
+// in four epilogue warps straight to global memory, or with vector reductions
+// (red.global.add.v4.f32) into a zeroed Y when SPLIT_K > 1.
+//
+// Persistent: one CTA per (SM x resident slot) walks the work units
+// (tile, k-slice) round-robin.  The TMEM accumulator is double-buffered
+// (2 x BN columns), so the epilogue of unit i overlaps the MMAs of unit i+1 and
+// the TMA ring never drains between units.
 //
 // Implicit GEMM (TQ > 0): a 128-row M tile is a TP x TQ rectangle of output
 // pixels of one image (TP = 128 / TQ).  For filter tap (r, s) and channel block
@@ -33,7 +38,7 @@ struct TcCfg {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+    static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
     static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
     static constexpr int THREADS = 192;
 };
@@ -41,13 +46,32 @@ struct TcCfg {
 struct TcParams {
     int M, N, K;  // GEMM view (conv: M = N*P*Q, N = K_out, K = R*S*C)
     int kblocks, kb_per_split, split;
+    int m_tiles, n_tiles, batch;  // GEMM tiles per batch (conv: m_tiles = images x pixel tiles)
+    int units;                    // batch * m_tiles * n_tiles * split
     float* C;
-    long long sC;
     // implicit GEMM
     int P, Q, S, CB;  // CB = channel blocks of BK per tap
     int sh, sw, ph, pw, dh, dw;
     int tiles_p, tiles_q;
 };
+
+struct Unit {
+    int bz, mt, nt, kb0, nkb;
+};
+
+__device__ __forceinline__ Unit decode_unit(const TcParams& p, int u) {
+    Unit w;
+    const int kz = u % p.split;
+    int t = u / p.split;
+    w.mt = t % p.m_tiles;  // m fastest: concurrent CTAs share the B (weight) tile in L2
+    t /= p.m_tiles;
+    w.nt = t % p.n_tiles;
+    w.bz = t / p.n_tiles;
+    // balanced k slices: every slice is non-empty when split <= kblocks (static validity)
+    w.kb0 = (int)((long long)kz * p.kblocks / p.split);
+    w.nkb = (int)((long long)(kz + 1) * p.kblocks / p.split) - w.kb0;
+    return w;
+}
 
 template <int BN, int BK, int STAGES, int TQ>
 __global__ void __launch_bounds__(192, 1)
@@ -62,34 +86,21 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + STAGES * Cfg::STAGE_BYTES);
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
-    uint64_t* tmem_full = bars + 2 * STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+    uint64_t* acc_full = bars + 2 * STAGES;       // [2] MMA -> epilogue
+    uint64_t* acc_empty = bars + 2 * STAGES + 2;  // [2] epilogue -> MMA
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.y * BN;
-    const int bz = blockIdx.z / p.split, kz = blockIdx.z % p.split;
-    const int kb0 = kz * p.kb_per_split;
-    const int kb1 = min(p.kblocks, kb0 + p.kb_per_split);
-    const int nkb = kb1 - kb0;
-    if (nkb <= 0) return;  // uniform per CTA, before any barrier
-    // M tile: rows m0.. (GEMM) or the pixel rectangle (img, p0.., q0..) (conv)
-    int m0 = 0, img = bz, p0 = 0, q0 = 0;
-    if constexpr (CONV) {
-        const int bx = blockIdx.x;
-        q0 = (bx % p.tiles_q) * TQ;
-        const int t = bx / p.tiles_q;
-        p0 = (t % p.tiles_p) * TP;
-        img = t / p.tiles_p;
-    } else {
-        m0 = blockIdx.x * BM;
-    }
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             tc::mbar_init(tc::smem_u32(&full[s]), 1);
             tc::mbar_init(tc::smem_u32(&empty[s]), 1);
         }
-        tc::mbar_init(tc::smem_u32(tmem_full), 1);
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(tc::smem_u32(&acc_full[a]), 1);
+            tc::mbar_init(tc::smem_u32(&acc_empty[a]), 4);  // one arrive per epilogue warp
+        }
         tc::fence_barrier_init();
         tc::tma_prefetch(&tmA);
         tc::tma_prefetch(&tmB);
@@ -101,34 +112,46 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---- TMA producer
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-                tc::mbar_wait(tc::smem_u32(&empty[s]), ph ^ 1u);
-                const uint32_t fb = tc::smem_u32(&full[s]);
-                tc::mbar_expect_tx(fb, Cfg::STAGE_BYTES);
-                const uint32_t sa = tc::smem_u32(base + s * Cfg::STAGE_BYTES);
-                const uint32_t sb = sa + Cfg::A_BYTES;
-                const int kb = kb0 + i;
+        if (lane == 0) {  // ---- TMA producer: one continuous ring across units
+            int it = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                const Unit w = decode_unit(p, u);
+                int img = w.bz, p0 = 0, q0 = 0;
                 if constexpr (CONV) {
-                    const int cb = kb % p.CB;
-                    const int rs = kb / p.CB;
-                    const int fs = rs % p.S, fr = rs / p.S;
-                    const int wq = q0 * p.sw - p.pw + fs * p.dw;
-                    const int hp = p0 * p.sh - p.ph + fr * p.dh;
+                    q0 = (w.mt % p.tiles_q) * TQ;
+                    const int t = w.mt / p.tiles_q;
+                    p0 = (t % p.tiles_p) * TP;
+                    img = t / p.tiles_p;
+                }
+                const int n0 = w.nt * BN;
+                for (int i = 0; i < w.nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+                    tc::mbar_wait(tc::smem_u32(&empty[s]), ph ^ 1u);
+                    const uint32_t fb = tc::smem_u32(&full[s]);
+                    tc::mbar_expect_tx(fb, Cfg::STAGE_BYTES);
+                    const uint32_t sa = tc::smem_u32(base + s * Cfg::STAGE_BYTES);
+                    const uint32_t sb = sa + Cfg::A_BYTES;
+                    const int kb = w.kb0 + i;
+                    if constexpr (CONV) {
+                        const int cb = kb % p.CB;
+                        const int rs = kb / p.CB;
+                        const int fs = rs % p.S, fr = rs / p.S;
+                        const int wq = q0 * p.sw - p.pw + fs * p.dw;
+                        const int hp = p0 * p.sh - p.ph + fr * p.dh;
 #pragma unroll
-                    for (int a = 0; a < BK / 64; ++a) {
-                        const int c0 = cb * BK + a * 64;
-                        tc::tma_load_4d(sa + a * BM * 128, &tmA, fb, c0, wq, hp, img);
-                        tc::tma_load_4d(sb + a * BN * 128, &tmB, fb, c0, fs, fr, n0);
-                    }
-                } else {
-                    const int k0 = kb * BK;
+                        for (int a = 0; a < BK / 64; ++a) {
+                            const int c0 = cb * BK + a * 64;
+                            tc::tma_load_4d(sa + a * BM * 128, &tmA, fb, c0, wq, hp, img);
+                            tc::tma_load_4d(sb + a * BN * 128, &tmB, fb, c0, fs, fr, n0);
+                        }
+                    } else {
+                        const int k0 = kb * BK;
 #pragma unroll
-                    for (int a = 0; a < BK / 64; ++a) {
-                        tc::tma_load_3d(sa + a * BM * 128, &tmA, fb, k0 + a * 64, m0, bz);
-                        tc::tma_load_3d(sb + a * BN * 128, &tmB, fb, k0 + a * 64, n0, bz);
+                        for (int a = 0; a < BK / 64; ++a) {
+                            tc::tma_load_3d(sa + a * BM * 128, &tmA, fb, k0 + a * 64, w.mt * BM, w.bz);
+                            tc::tma_load_3d(sb + a * BN * 128, &tmB, fb, k0 + a * 64, n0, w.bz);
+                        }
                     }
                 }
             }
@@ -136,65 +159,86 @@ __global__ void __launch_bounds__(192, 1)
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer
             constexpr uint32_t idesc = tc::idesc_bf16(BM, BN);
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-                tc::mbar_wait(tc::smem_u32(&full[s]), ph);
+            int it = 0, j = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+                const Unit w = decode_unit(p, u);
+                const int a = j & 1;
+                tc::mbar_wait(tc::smem_u32(&acc_empty[a]), ((uint32_t)(j >> 1) & 1u) ^ 1u);
                 tc::tc_fence_after();
-                const uint32_t sa = tc::smem_u32(base + s * Cfg::STAGE_BYTES);
-                const uint32_t sb = sa + Cfg::A_BYTES;
+                const uint32_t acc = tmem + (uint32_t)(a * BN);
+                for (int i = 0; i < w.nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+                    tc::mbar_wait(tc::smem_u32(&full[s]), ph);
+                    tc::tc_fence_after();
+                    const uint32_t sa = tc::smem_u32(base + s * Cfg::STAGE_BYTES);
+                    const uint32_t sb = sa + Cfg::A_BYTES;
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    const uint32_t atom = k / 4, inner = (k % 4) * 32;
-                    const uint64_t da = tc::sdesc_sw128(sa + atom * BM * 128 + inner);
-                    const uint64_t db = tc::sdesc_sw128(sb + atom * BN * 128 + inner);
-                    tc::umma_bf16(tmem, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint32_t atom = k / 4, inner = (k % 4) * 32;
+                        const uint64_t da = tc::sdesc_sw128(sa + atom * BM * 128 + inner);
+                        const uint64_t db = tc::sdesc_sw128(sb + atom * BN * 128 + inner);
+                        tc::umma_bf16(acc, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                    }
+                    tc::umma_commit(tc::smem_u32(&empty[s]));  // frees the stage when these MMAs finish
                 }
-                tc::umma_commit(tc::smem_u32(&empty[s]));  // frees the stage when these MMAs finish
+                tc::umma_commit(tc::smem_u32(&acc_full[a]));  // accumulator ready for the epilogue
             }
-            tc::umma_commit(tc::smem_u32(tmem_full));
         }
     } else {  // ---- epilogue: TMEM -> registers -> global
         const int q = warp & 3;
         const int trow = q * 32 + lane;  // row of the 128-row tile held by this thread
-        bool row_ok;
-        long long orow;                  // output row index (GEMM row or NPQ pixel)
-        if constexpr (CONV) {
-            const int pp = p0 + trow / TQ, qq = q0 + trow % TQ;
-            row_ok = pp < p.P && qq < p.Q;
-            orow = ((long long)img * p.P + pp) * p.Q + qq;
-        } else {
-            row_ok = m0 + trow < p.M;
-            orow = (long long)bz * p.M + m0 + trow;
-        }
-        tc::mbar_wait(tc::smem_u32(tmem_full), 0);
-        tc::tc_fence_after();
-        float* crow = p.C + orow * p.N;
         const bool vec_ok = (p.N % 4) == 0;
-#pragma unroll 1
-        for (int c = 0; c < BN / 16; ++c) {
-            uint32_t r[16];
-            tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 16), r);
-            tc::tmem_ld_wait();
-            const int n = n0 + c * 16;
-            if (!row_ok || n >= p.N) continue;
-            if (vec_ok && n + 16 <= p.N) {
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    float4 f = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                           __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-                    if (p.split > 1) tc::red_add_v4(crow + n + 4 * v, f.x, f.y, f.z, f.w);
-                    else *reinterpret_cast<float4*>(crow + n + 4 * v) = f;
-                }
+        int j = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+            const Unit w = decode_unit(p, u);
+            const int a = j & 1;
+            bool row_ok;
+            long long orow;  // output row index (GEMM row or NPQ pixel)
+            if constexpr (CONV) {
+                const int q0 = (w.mt % p.tiles_q) * TQ;
+                const int t = w.mt / p.tiles_q;
+                const int pp = (t % p.tiles_p) * TP + trow / TQ, qq = q0 + trow % TQ;
+                const int img = t / p.tiles_p;
+                row_ok = pp < p.P && qq < p.Q;
+                orow = ((long long)img * p.P + pp) * p.Q + qq;
             } else {
+                const int m = w.mt * BM + trow;
+                row_ok = m < p.M;
+                orow = (long long)w.bz * p.M + m;
+            }
+            tc::mbar_wait(tc::smem_u32(&acc_full[a]), (uint32_t)(j >> 1) & 1u);
+            tc::tc_fence_after();
+            float* crow = p.C + orow * p.N;
+            const int n0 = w.nt * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN / 16; ++c) {
+                uint32_t r[16];
+                tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + c * 16), r);
+                tc::tmem_ld_wait();
+                const int n = n0 + c * 16;
+                if (!row_ok || n >= p.N) continue;
+                if (vec_ok && n + 16 <= p.N) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    if (n + j < p.N) {
-                        if (p.split > 1) atomicAdd(crow + n + j, __uint_as_float(r[j]));
-                        else crow[n + j] = __uint_as_float(r[j]);
+                    for (int v = 0; v < 4; ++v) {
+                        float4 f = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                               __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+                        if (p.split > 1) tc::red_add_v4(crow + n + 4 * v, f.x, f.y, f.z, f.w);
+                        else *reinterpret_cast<float4*>(crow + n + 4 * v) = f;
+                    }
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        if (n + jj < p.N) {
+                            if (p.split > 1) atomicAdd(crow + n + jj, __uint_as_float(r[jj]));
+                            else crow[n + jj] = __uint_as_float(r[jj]);
+                        }
                     }
                 }
             }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&acc_empty[a]));  // this warp's lanes are drained
         }
     }
     tc::tc_fence_before();
@@ -259,8 +303,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     p.M = (int)s.M; p.N = (int)s.N; p.K = (int)s.K;
     p.split = c.split;
     p.C = (float*)c.y;
-    p.sC = s.M * s.N;
-    dim3 grid;
+    p.n_tiles = (int)((s.N + BN - 1) / BN);
     if constexpr (CONV) {
         constexpr int TP = 128 / TQ;
         // X: NHWC as {C, W, H, N}, traversal strides (1, sw, sh, 1); box {64, TQ*sw, TP*sh, 1}
@@ -281,21 +324,32 @@ cudaError_t tc_launch(const LaunchCtx& c) {
         p.tiles_q = (int)((s.q + TQ - 1) / TQ);
         p.tiles_p = (int)((s.p + TP - 1) / TP);
         p.kblocks = (int)(s.r * s.s) * p.CB;
-        grid = dim3((unsigned)(s.n * p.tiles_p * p.tiles_q), (unsigned)((s.N + BN - 1) / BN), (unsigned)c.split);
+        p.m_tiles = (int)s.n * p.tiles_p * p.tiles_q;
+        p.batch = 1;
     } else {
         if (!make_kmajor_map(&ta, c.x, s.batch, s.M, s.K, Cfg::BM) ||
             !make_kmajor_map(&tb, c.w, s.batch, s.N, s.K, BN))
             return cudaErrorInvalidValue;
         p.kblocks = (int)((s.K + BK - 1) / BK);
-        grid = dim3((unsigned)((s.M + Cfg::BM - 1) / Cfg::BM), (unsigned)((s.N + BN - 1) / BN),
-                    (unsigned)(s.batch * c.split));
+        p.m_tiles = (int)((s.M + Cfg::BM - 1) / Cfg::BM);
+        p.batch = (int)s.batch;
     }
     p.kb_per_split = (p.kblocks + c.split - 1) / c.split;
+    const long long units = (long long)p.batch * p.m_tiles * p.n_tiles * c.split;
+    if (units >= (1ll << 31)) return cudaErrorInvalidValue;
+    p.units = (int)units;
     if (c.split > 1) {
         cudaError_t e = cudaMemsetAsync(c.y, 0, (size_t)s.y_elems * sizeof(float), c.stream);
         if (e != cudaSuccess) return e;
     }
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM, c.stream>>>(ta, tb, p);
+    // persistent grid: SMs x resident CTAs (shared memory and TMEM limited)
+    int per_sm = (int)((228 * 1024) / (Cfg::SMEM + 1024));
+    per_sm = per_sm < 1 ? 1 : per_sm;
+    const int tmem_per_sm = (int)(512 / Cfg::TMEM_COLS);
+    per_sm = per_sm < tmem_per_sm ? per_sm : tmem_per_sm;
+    long long grid = (long long)c.num_sms * per_sm;
+    if (grid > units) grid = units;
+    kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, c.stream>>>(ta, tb, p);
     count_launches(1);
     return cudaGetLastError();
 }
