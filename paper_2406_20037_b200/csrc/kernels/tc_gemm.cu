@@ -3,20 +3,26 @@
 //   dense / bmm : Y[b,m,n] (fp32) = sum_k X[b,m,k] W[b,n,k],  X, W bf16
 //   conv2d      : Y[n,p,q,k] (fp32) = sum_{r,s,c} X[n,p*sh-ph+r*dh,q*sw-pw+s*dw,c] W[k,r,s,c]
 //
-// The sketch (Def. 2.1): tile the output into 128 x BN tiles (x SPLIT_K slices of
+// The sketch (Def. 2.1): tile the output into BM x BN tiles (x SPLIT_K slices of
 // the reduction); stage BK-wide reduction slices of A and B through a
 // STAGES-deep shared-memory ring filled by TMA (128-byte swizzle, one mbarrier
 // pair per stage); accumulate in TMEM with tcgen05.mma issued by one thread
-// (UMMA 128 x BN x 16, kind::f16, fp32 accumulate); drain TMEM with tcgen05.ld
-// in four epilogue warps straight to global memory, or with vector reductions
+// (kind::f16, fp32 accumulate); drain TMEM with tcgen05.ld in four epilogue
+// warps straight to global memory, or with vector reductions
 // (red.global.add.v4.f32) into a zeroed Y when SPLIT_K > 1.
 //
-// Persistent: one CTA per (SM x resident slot) walks the work units
+// BM = 128: one CTA per tile, UMMA 128 x BN x 16 (cta_group::1).
+// BM = 256: a CTA pair (cluster of 2 on one TPC) per tile, UMMA 256 x BN x 16
+// (cta_group::2): each CTA stages 128 rows of A and BN/2 rows of B, the leader
+// issues the MMA over both CTAs' shared memory, and each CTA's TMEM holds its
+// 128 accumulator rows — half the B traffic per SM of two 1-CTA tiles.
+//
+// Persistent: one CTA (pair) per SM (pair) slot walks the work units
 // (tile, k-slice) round-robin.  The TMEM accumulator is double-buffered
 // (2 x BN columns), so the epilogue of unit i overlaps the MMAs of unit i+1 and
 // the TMA ring never drains between units.
 //
-// Implicit GEMM (TQ > 0): a 128-row M tile is a TP x TQ rectangle of output
+// Implicit GEMM (TQ > 0): a 128-row M sub-tile is a TP x TQ rectangle of output
 // pixels of one image (TP = 128 / TQ).  For filter tap (r, s) and channel block
 // c0 its A slice is ONE 4-D TMA box of X (NHWC) starting at
 // (c0, q0*sw - pw + s*dw, p0*sh - ph + r*dh, n) with traversal strides (sw, sh):
@@ -24,7 +30,7 @@
 // (out-of-bounds fill).  B is W (KRSC) as a 4-D box (c0, s, r, k0).
 // Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
 // warps 2..5 = epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).
-// Knobs: BM (128), BN, BK, STAGES, SPLIT_K, TILE_Q (conv only).
+// Knobs: BM, BN, BK, STAGES, SPLIT_K, TILE_Q (conv only).
 #include <cstring>
 
 #include "common.cuh"
@@ -32,11 +38,12 @@
 
 namespace db200 {
 
-template <int BN, int BK, int STAGES>
+template <int BN, int BK, int STAGES, int CG>
 struct TcCfg {
-    static constexpr int BM = 128;
+    static constexpr int BM = 128;  // rows of A per CTA
+    static constexpr int BNC = BN / CG;  // rows of B per CTA
     static constexpr int A_BYTES = BM * BK * 2;
-    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int B_BYTES = BNC * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
     static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
@@ -45,9 +52,10 @@ struct TcCfg {
 
 struct TcParams {
     int M, N, K;  // GEMM view (conv: M = N*P*Q, N = K_out, K = R*S*C)
-    int kblocks, kb_per_split, split;
-    int m_tiles, n_tiles, batch;  // GEMM tiles per batch (conv: m_tiles = images x pixel tiles)
-    int units;                    // batch * m_tiles * n_tiles * split
+    int kblocks, split;
+    int m_tiles;                  // 128-row sub-tiles per batch (conv: images x pixel tiles)
+    int mp_tiles, n_tiles, batch;  // tiles of the CTA group (CG sub-tiles each)
+    int units;                    // batch * mp_tiles * n_tiles * split
     float* C;
     // implicit GEMM
     int P, Q, S, CB;  // CB = channel blocks of BK per tap
@@ -56,15 +64,15 @@ struct TcParams {
 };
 
 struct Unit {
-    int bz, mt, nt, kb0, nkb;
+    int bz, mt, nt, kb0, nkb;  // mt = index of the CTA group's tile
 };
 
 __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u) {
     Unit w;
     const int kz = u % p.split;
     int t = u / p.split;
-    w.mt = t % p.m_tiles;  // m fastest: concurrent CTAs share the B (weight) tile in L2
-    t /= p.m_tiles;
+    w.mt = t % p.mp_tiles;  // m fastest: concurrent CTAs share the B (weight) tile in L2
+    t /= p.mp_tiles;
     w.nt = t % p.n_tiles;
     w.bz = t / p.n_tiles;
     // balanced k slices: every slice is non-empty when split <= kblocks (static validity)
@@ -73,11 +81,11 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u) {
     return w;
 }
 
-template <int BN, int BK, int STAGES, int TQ>
+template <int BN, int BK, int STAGES, int TQ, int CG>
 __global__ void __launch_bounds__(192, 1)
     tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const TcParams p) {
-    using Cfg = TcCfg<BN, BK, STAGES>;
+    using Cfg = TcCfg<BN, BK, STAGES, CG>;
     constexpr int BM = Cfg::BM;
     constexpr bool CONV = TQ > 0;
     constexpr int TP = CONV ? BM / TQ : 1;
@@ -91,45 +99,56 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? tc::cluster_ctarank() : 0u;
+    const int group = blockIdx.x / CG, ngroups = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            tc::mbar_init(tc::smem_u32(&full[s]), 1);
+            tc::mbar_init(tc::smem_u32(&full[s]), CG);  // leader: own arrive.expect_tx (+ the peer's arrive)
             tc::mbar_init(tc::smem_u32(&empty[s]), 1);
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(tc::smem_u32(&acc_full[a]), 1);
-            tc::mbar_init(tc::smem_u32(&acc_empty[a]), 4);  // one arrive per epilogue warp
+            tc::mbar_init(tc::smem_u32(&acc_empty[a]), 4 * CG);  // one arrive per epilogue warp of the group
         }
         tc::fence_barrier_init();
         tc::tma_prefetch(&tmA);
         tc::tma_prefetch(&tmB);
     }
-    if (warp == 1) tc::tmem_alloc<Cfg::TMEM_COLS>(tc::smem_u32(tmem_slot));
+    if (warp == 1) {
+        if constexpr (CG == 2) tc::tmem_alloc_cg2<Cfg::TMEM_COLS>(tc::smem_u32(tmem_slot));
+        else tc::tmem_alloc<Cfg::TMEM_COLS>(tc::smem_u32(tmem_slot));
+    }
     tc::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) tc::cluster_sync();
+    else __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+
+    // this CTA's 128-row sub-tile of the group's tile
+    auto sub_tile = [&](const Unit& w) { return w.mt * CG + (int)rank; };
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer: one continuous ring across units
             int it = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            for (int u = group; u < p.units; u += ngroups) {
                 const Unit w = decode_unit(p, u);
+                const int mt = sub_tile(w);
                 int img = w.bz, p0 = 0, q0 = 0;
                 if constexpr (CONV) {
-                    q0 = (w.mt % p.tiles_q) * TQ;
-                    const int t = w.mt / p.tiles_q;
+                    q0 = (mt % p.tiles_q) * TQ;
+                    const int t = mt / p.tiles_q;
                     p0 = (t % p.tiles_p) * TP;
-                    img = t / p.tiles_p;
+                    img = t / p.tiles_p;  // >= N for a padding sub-tile: TMA zero-fills it
                 }
-                const int n0 = w.nt * BN;
+                const int nb = w.nt * BN + (int)rank * Cfg::BNC;
                 for (int i = 0; i < w.nkb; ++i, ++it) {
                     const int s = it % STAGES;
                     const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
                     tc::mbar_wait(tc::smem_u32(&empty[s]), ph ^ 1u);
                     const uint32_t fb = tc::smem_u32(&full[s]);
-                    tc::mbar_expect_tx(fb, Cfg::STAGE_BYTES);
+                    if (rank == 0) tc::mbar_expect_tx(fb, CG * Cfg::STAGE_BYTES);
+                    else tc::mbar_arrive_remote(fb, 0);
                     const uint32_t sa = tc::smem_u32(base + s * Cfg::STAGE_BYTES);
                     const uint32_t sb = sa + Cfg::A_BYTES;
                     const int kb = w.kb0 + i;
@@ -142,25 +161,35 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                         for (int a = 0; a < BK / 64; ++a) {
                             const int c0 = cb * BK + a * 64;
-                            tc::tma_load_4d(sa + a * BM * 128, &tmA, fb, c0, wq, hp, img);
-                            tc::tma_load_4d(sb + a * BN * 128, &tmB, fb, c0, fs, fr, n0);
+                            if constexpr (CG == 2) {
+                                tc::tma_load_4d_cg2(sa + a * BM * 128, &tmA, fb, c0, wq, hp, img);
+                                tc::tma_load_4d_cg2(sb + a * Cfg::BNC * 128, &tmB, fb, c0, fs, fr, nb);
+                            } else {
+                                tc::tma_load_4d(sa + a * BM * 128, &tmA, fb, c0, wq, hp, img);
+                                tc::tma_load_4d(sb + a * Cfg::BNC * 128, &tmB, fb, c0, fs, fr, nb);
+                            }
                         }
                     } else {
                         const int k0 = kb * BK;
 #pragma unroll
                         for (int a = 0; a < BK / 64; ++a) {
-                            tc::tma_load_3d(sa + a * BM * 128, &tmA, fb, k0 + a * 64, w.mt * BM, w.bz);
-                            tc::tma_load_3d(sb + a * BN * 128, &tmB, fb, k0 + a * 64, n0, w.bz);
+                            if constexpr (CG == 2) {
+                                tc::tma_load_3d_cg2(sa + a * BM * 128, &tmA, fb, k0 + a * 64, mt * BM, w.bz);
+                                tc::tma_load_3d_cg2(sb + a * Cfg::BNC * 128, &tmB, fb, k0 + a * 64, nb, w.bz);
+                            } else {
+                                tc::tma_load_3d(sa + a * BM * 128, &tmA, fb, k0 + a * 64, mt * BM, w.bz);
+                                tc::tma_load_3d(sb + a * Cfg::BNC * 128, &tmB, fb, k0 + a * 64, nb, w.bz);
+                            }
                         }
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer
-            constexpr uint32_t idesc = tc::idesc_bf16(BM, BN);
+        if (lane == 0 && rank == 0) {  // ---- MMA issuer (the leader CTA of a pair)
+            constexpr uint32_t idesc = tc::idesc_bf16(BM * CG, BN);
             int it = 0, j = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+            for (int u = group; u < p.units; u += ngroups, ++j) {
                 const Unit w = decode_unit(p, u);
                 const int a = j & 1;
                 tc::mbar_wait(tc::smem_u32(&acc_empty[a]), ((uint32_t)(j >> 1) & 1u) ^ 1u);
@@ -177,75 +206,91 @@ __global__ void __launch_bounds__(192, 1)
                     for (int k = 0; k < BK / 16; ++k) {
                         const uint32_t atom = k / 4, inner = (k % 4) * 32;
                         const uint64_t da = tc::sdesc_sw128(sa + atom * BM * 128 + inner);
-                        const uint64_t db = tc::sdesc_sw128(sb + atom * BN * 128 + inner);
-                        tc::umma_bf16(acc, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                        const uint64_t db = tc::sdesc_sw128(sb + atom * Cfg::BNC * 128 + inner);
+                        if constexpr (CG == 2) tc::umma_bf16_cg2(acc, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                        else tc::umma_bf16(acc, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
                     }
-                    tc::umma_commit(tc::smem_u32(&empty[s]));  // frees the stage when these MMAs finish
+                    // frees the stage (in both CTAs of a pair) when these MMAs finish
+                    if constexpr (CG == 2) tc::umma_commit_cg2(tc::smem_u32(&empty[s]));
+                    else tc::umma_commit(tc::smem_u32(&empty[s]));
                 }
-                tc::umma_commit(tc::smem_u32(&acc_full[a]));  // accumulator ready for the epilogue
+                if constexpr (CG == 2) tc::umma_commit_cg2(tc::smem_u32(&acc_full[a]));
+                else tc::umma_commit(tc::smem_u32(&acc_full[a]));
             }
         }
     } else {  // ---- epilogue: TMEM -> registers -> global
         const int q = warp & 3;
-        const int trow = q * 32 + lane;  // row of the 128-row tile held by this thread
+        const int trow = q * 32 + lane;  // row of the 128-row sub-tile held by this thread
         const bool vec_ok = (p.N % 4) == 0;
         int j = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+        for (int u = group; u < p.units; u += ngroups, ++j) {
             const Unit w = decode_unit(p, u);
+            const int mt = sub_tile(w);
             const int a = j & 1;
-            bool row_ok;
+            bool row_ok = mt < p.m_tiles;
             long long orow;  // output row index (GEMM row or NPQ pixel)
             if constexpr (CONV) {
-                const int q0 = (w.mt % p.tiles_q) * TQ;
-                const int t = w.mt / p.tiles_q;
+                const int q0 = (mt % p.tiles_q) * TQ;
+                const int t = mt / p.tiles_q;
                 const int pp = (t % p.tiles_p) * TP + trow / TQ, qq = q0 + trow % TQ;
                 const int img = t / p.tiles_p;
-                row_ok = pp < p.P && qq < p.Q;
+                row_ok = row_ok && pp < p.P && qq < p.Q;
                 orow = ((long long)img * p.P + pp) * p.Q + qq;
             } else {
-                const int m = w.mt * BM + trow;
-                row_ok = m < p.M;
+                const int m = mt * BM + trow;
+                row_ok = row_ok && m < p.M;
                 orow = (long long)w.bz * p.M + m;
             }
             tc::mbar_wait(tc::smem_u32(&acc_full[a]), (uint32_t)(j >> 1) & 1u);
             tc::tc_fence_after();
             float* crow = p.C + orow * p.N;
             const int n0 = w.nt * BN;
+            constexpr int CH = BN < 64 ? BN : 64;  // columns per TMEM drain: several loads, one wait
 #pragma unroll 1
-            for (int c = 0; c < BN / 16; ++c) {
-                uint32_t r[16];
-                tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + c * 16), r);
+            for (int c0 = 0; c0 < BN; c0 += CH) {
+                uint32_t r[CH / 16][16];
+#pragma unroll
+                for (int g = 0; g < CH / 16; ++g)
+                    tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + c0 + g * 16), r[g]);
                 tc::tmem_ld_wait();
-                const int n = n0 + c * 16;
-                if (!row_ok || n >= p.N) continue;
-                if (vec_ok && n + 16 <= p.N) {
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        float4 f = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                               __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-                        if (p.split > 1) tc::red_add_v4(crow + n + 4 * v, f.x, f.y, f.z, f.w);
-                        else *reinterpret_cast<float4*>(crow + n + 4 * v) = f;
-                    }
-                } else {
+                for (int g = 0; g < CH / 16; ++g) {
+                    const int n = n0 + c0 + g * 16;
+                    if (!row_ok || n >= p.N) continue;
+                    if (vec_ok && n + 16 <= p.N) {
 #pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) {
-                        if (n + jj < p.N) {
-                            if (p.split > 1) atomicAdd(crow + n + jj, __uint_as_float(r[jj]));
-                            else crow[n + jj] = __uint_as_float(r[jj]);
+                        for (int v = 0; v < 4; ++v) {
+                            float4 f = make_float4(__uint_as_float(r[g][4 * v]), __uint_as_float(r[g][4 * v + 1]),
+                                                   __uint_as_float(r[g][4 * v + 2]), __uint_as_float(r[g][4 * v + 3]));
+                            if (p.split > 1) tc::red_add_v4(crow + n + 4 * v, f.x, f.y, f.z, f.w);
+                            else *reinterpret_cast<float4*>(crow + n + 4 * v) = f;
+                        }
+                    } else {
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) {
+                            if (n + jj < p.N) {
+                                if (p.split > 1) atomicAdd(crow + n + jj, __uint_as_float(r[g][jj]));
+                                else crow[n + jj] = __uint_as_float(r[g][jj]);
+                            }
                         }
                     }
                 }
             }
             tc::tc_fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&acc_empty[a]));  // this warp's lanes are drained
+            if (lane == 0) {  // this warp's accumulator lanes are drained
+                if constexpr (CG == 2) tc::mbar_arrive_remote(tc::smem_u32(&acc_empty[a]), 0);
+                else tc::mbar_arrive(tc::smem_u32(&acc_empty[a]));
+            }
         }
     }
     tc::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) tc::cluster_sync();
+    else __syncthreads();
     if (warp == 1) {
         tc::tc_fence_after();
-        tc::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
+        if constexpr (CG == 2) tc::tmem_dealloc_cg2<Cfg::TMEM_COLS>(tmem);
+        else tc::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
     }
 }
 
@@ -285,11 +330,11 @@ static bool make_kmajor_map(CUtensorMap* m, const void* ptr, int64_t batch, int6
     return encode(m, ptr, 3, dims, strides, box, es);
 }
 
-template <int BN, int BK, int STAGES, int TQ>
+template <int BN, int BK, int STAGES, int TQ, int CG>
 cudaError_t tc_launch(const LaunchCtx& c) {
-    using Cfg = TcCfg<BN, BK, STAGES>;
+    using Cfg = TcCfg<BN, BK, STAGES, CG>;
     constexpr bool CONV = TQ > 0;
-    auto kern = tc_gemm_bf16_kernel<BN, BK, STAGES, TQ>;
+    auto kern = tc_gemm_bf16_kernel<BN, BK, STAGES, TQ, CG>;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -311,10 +356,10 @@ cudaError_t tc_launch(const LaunchCtx& c) {
         cuuint64_t xs[3] = {(cuuint64_t)s.c * 2, (cuuint64_t)(s.w * s.c * 2), (cuuint64_t)(s.h * s.w * s.c * 2)};
         cuuint32_t xb[4] = {64, (cuuint32_t)(TQ * s.sw), (cuuint32_t)(TP * s.sh), 1};
         cuuint32_t xe[4] = {1, (cuuint32_t)s.sw, (cuuint32_t)s.sh, 1};
-        // W: KRSC as {C, S, R, K}; box {64, 1, 1, BN}
+        // W: KRSC as {C, S, R, K}; box {64, 1, 1, BN / CG}
         cuuint64_t wd[4] = {(cuuint64_t)s.c, (cuuint64_t)s.s, (cuuint64_t)s.r, (cuuint64_t)s.k};
         cuuint64_t ws[3] = {(cuuint64_t)s.c * 2, (cuuint64_t)(s.s * s.c * 2), (cuuint64_t)(s.r * s.s * s.c * 2)};
-        cuuint32_t wb[4] = {64, 1, 1, (cuuint32_t)BN};
+        cuuint32_t wb[4] = {64, 1, 1, (cuuint32_t)Cfg::BNC};
         cuuint32_t we[4] = {1, 1, 1, 1};
         if (!encode(&ta, c.x, 4, xd, xs, xb, xe) || !encode(&tb, c.w, 4, wd, ws, wb, we))
             return cudaErrorInvalidValue;
@@ -328,55 +373,68 @@ cudaError_t tc_launch(const LaunchCtx& c) {
         p.batch = 1;
     } else {
         if (!make_kmajor_map(&ta, c.x, s.batch, s.M, s.K, Cfg::BM) ||
-            !make_kmajor_map(&tb, c.w, s.batch, s.N, s.K, BN))
+            !make_kmajor_map(&tb, c.w, s.batch, s.N, s.K, Cfg::BNC))
             return cudaErrorInvalidValue;
         p.kblocks = (int)((s.K + BK - 1) / BK);
         p.m_tiles = (int)((s.M + Cfg::BM - 1) / Cfg::BM);
         p.batch = (int)s.batch;
     }
-    p.kb_per_split = (p.kblocks + c.split - 1) / c.split;
-    const long long units = (long long)p.batch * p.m_tiles * p.n_tiles * c.split;
+    p.mp_tiles = (p.m_tiles + CG - 1) / CG;
+    const long long units = (long long)p.batch * p.mp_tiles * p.n_tiles * c.split;
     if (units >= (1ll << 31)) return cudaErrorInvalidValue;
     p.units = (int)units;
     if (c.split > 1) {
         cudaError_t e = cudaMemsetAsync(c.y, 0, (size_t)s.y_elems * sizeof(float), c.stream);
         if (e != cudaSuccess) return e;
     }
-    // persistent grid: SMs x resident CTAs (shared memory and TMEM limited)
+    // persistent grid: CTA groups = SMs / CG x resident slots (shared memory and TMEM limited)
     int per_sm = (int)((228 * 1024) / (Cfg::SMEM + 1024));
     per_sm = per_sm < 1 ? 1 : per_sm;
     const int tmem_per_sm = (int)(512 / Cfg::TMEM_COLS);
     per_sm = per_sm < tmem_per_sm ? per_sm : tmem_per_sm;
-    long long grid = (long long)c.num_sms * per_sm;
-    if (grid > units) grid = units;
-    kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, c.stream>>>(ta, tb, p);
+    long long groups = (long long)(c.num_sms / CG) * per_sm;
+    if (groups > units) groups = units;
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)(groups * CG));
+    cfg.blockDim = dim3(Cfg::THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
     count_launches(1);
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-constexpr bool tc_static_ok(int BN, int BK, int STAGES) {
-    return 1024 + (size_t)STAGES * (128 + BN) * BK * 2 + 256 <= 227 * 1024;
+constexpr bool tc_static_ok(int BN, int BK, int STAGES, int CG) {
+    return 1024 + (size_t)STAGES * (128 + BN / CG) * BK * 2 + 256 <= 227 * 1024;
 }
 
-template <int BN, int BK, int STAGES, int TQ>
+template <int BN, int BK, int STAGES, int TQ, int CG>
 void tc_register() {
-    if constexpr (tc_static_ok(BN, BK, STAGES))
-        registry_add(kernel_key(TQ ? SK_TC_IGEMM_CONV_BF16 : SK_TC_GEMM_BF16, 128, BN, BK, STAGES, TQ),
-                     &tc_launch<BN, BK, STAGES, TQ>);
+    if constexpr (tc_static_ok(BN, BK, STAGES, CG))
+        registry_add(kernel_key(TQ ? SK_TC_IGEMM_CONV_BF16 : SK_TC_GEMM_BF16, 128 * CG, BN, BK, STAGES, TQ),
+                     &tc_launch<BN, BK, STAGES, TQ, CG>);
 }
 
-#define TC_STAGES(BN, BK, TQ)                                                                         \
-    tc_register<BN, BK, 2, TQ>(); tc_register<BN, BK, 3, TQ>(); tc_register<BN, BK, 4, TQ>(); \
-    tc_register<BN, BK, 6, TQ>();
-#define TC_SHAPES(TQ) \
-    TC_STAGES(64, 64, TQ) TC_STAGES(128, 64, TQ) TC_STAGES(256, 64, TQ) TC_STAGES(64, 128, TQ) \
-    TC_STAGES(128, 128, TQ) TC_STAGES(256, 128, TQ)
+#define TC_STAGES(BN, BK, TQ, CG)                                                                            \
+    tc_register<BN, BK, 2, TQ, CG>(); tc_register<BN, BK, 3, TQ, CG>(); tc_register<BN, BK, 4, TQ, CG>(); \
+    tc_register<BN, BK, 6, TQ, CG>();
+#define TC_SHAPES(TQ, CG)                                                                        \
+    TC_STAGES(64, 64, TQ, CG) TC_STAGES(128, 64, TQ, CG) TC_STAGES(256, 64, TQ, CG)             \
+    TC_STAGES(64, 128, TQ, CG) TC_STAGES(128, 128, TQ, CG) TC_STAGES(256, 128, TQ, CG)
 
 void register_tc_gemm() {
-    TC_SHAPES(0)   // dense / bmm
-    TC_SHAPES(8)   // conv, 16 x 8 pixel tiles
-    TC_SHAPES(16)  // conv, 8 x 16
-    TC_SHAPES(32)  // conv, 4 x 32
+    TC_SHAPES(0, 1) TC_SHAPES(0, 2)     // dense / bmm
+    TC_SHAPES(8, 1) TC_SHAPES(8, 2)     // conv, 16 x 8 pixel sub-tiles
+    TC_SHAPES(16, 1) TC_SHAPES(16, 2)   // conv, 8 x 16
+    TC_SHAPES(32, 1) TC_SHAPES(32, 2)   // conv, 4 x 32
 }
 
 }  // namespace db200

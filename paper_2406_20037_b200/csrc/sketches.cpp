@@ -25,7 +25,8 @@ static std::vector<SketchDesc> build_catalogue() {
     // BK staged by TMA with 128-byte swizzle, STAGES-deep mbarrier pipeline,
     // split-K (runtime).
     const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K"};
-    const std::vector<std::vector<int32_t>> tc_vals = {{128}, {64, 128, 256}, {64, 128}, {2, 3, 4, 6}, {1, 2, 4}};
+    // BM = 256 is the CTA-pair schedule (cta_group::2, UMMA M = 256 over two SMs).
+    const std::vector<std::vector<int32_t>> tc_vals = {{128, 256}, {64, 128, 256}, {64, 128}, {2, 3, 4, 6}, {1, 2, 4}};
     c.push_back({SK_TC_GEMM_BF16, "tc_gemm_bf16", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL), TUNER_BF16,
                  tc_names, tc_vals});
     // implicit-GEMM conv: the 128-row M tile is a (128/TILE_Q) x TILE_Q rectangle of output pixels
@@ -119,9 +120,10 @@ static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
         if (sh.K % 8) return false;
         ktiles = (sh.K + bk - 1) / bk;
     }
-    const int64_t smem = (int64_t)stages * (bm + bn) * bk * 2 + 1024 /*align*/ + 256 /*barriers*/;
+    if (bn > 256 || (bm != 128 && bm != 256)) return false;
+    const int cg = bm / 128;  // CTAs per tile: each stages 128 rows of A and bn/cg rows of B
+    const int64_t smem = (int64_t)stages * (128 + bn / cg) * bk * 2 + 1024 /*align*/ + 256 /*barriers*/;
     if (smem > 227 * 1024) return false;
-    if (bn > 256 || bm != 128) return false;
     if (split > ktiles) return false;
     if ((int64_t)split * sh.batch > 65535) return false;
     return true;
