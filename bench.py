@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--n-sample", type=int, default=300)
     ap.add_argument("--droplet-budget", type=int, default=100)
     ap.add_argument("--baseline", type=int, default=10000)
-    ap.add_argument("--early-cut", type=float, default=20.0)
+    ap.add_argument("--early-cut", type=float, default=4.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--json-out", default=None)

@@ -5,12 +5,17 @@
 //
 // One rank's share of a batch goes through two pipelined phases on the
 // tuner's stream, with ONE host synchronisation per phase (not per candidate):
-//   1. verify: poison y (NaN), launch the candidate between two events, reduce
-//      max_err into a device slot (verify_maxerr); D2H all slots; sync.
+//   1. verify: one untimed launch, poison y (NaN), launch the candidate
+//      between two events (t_verify), reduce max_err into a device slot
+//      (verify_maxerr); D2H all slots; sync.
 //   2. time:   for every candidate that verified, W untimed launches, then R
-//      repeats of a CUDA graph of `number` back-to-back launches, each repeat
-//      bracketed by events (number = 20 us / t_verify, clamped to [1, 100]);
-//      sync; cost = median over repeats of elapsed / number (R-M2).
+//      repeats of `number` back-to-back launches (a CUDA graph of <= 8
+//      launches replayed), each repeat bracketed by events (number =
+//      20 us / t_verify, clamped to [1, 100]); sync; cost = trimmed mean over
+//      repeats of elapsed / number (R-M2).
+// Early cut (opts.early_cut = f > 0, SURVEY d.5): a candidate with t_verify >
+// f x the best cost known is ranked by t_verify alone; one > 1.5x gets 3
+// repeats instead of R.  Candidates that can still win get the full R.
 // Graph capture and instantiation of candidate j+1 on the host overlap the
 // GPU executing candidate j.
 #include <cuda_runtime.h>
@@ -28,6 +33,9 @@ cudaError_t launch_reference(const ShapeInfo& s, const void* x, const void* w, f
 cudaError_t launch_verify(const float* y, const float* r, const float* a, long long n, unsigned int* out,
                           int num_sms, cudaStream_t st);
 void set_capturing(bool on);
+
+static constexpr int kMaxGraphNodes = 8;     // launches per captured graph
+static constexpr double kLightFactor = 1.5;  // early-cut mode: > 1.5x the best -> 3 repeats
 
 static tuner_status cuda_fail(cudaError_t e, const char* what) {
     return fail(TUNER_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -165,10 +173,14 @@ struct GpuMeasurer : Measurer {
         CU(cudaMemsetAsync(d_err, 0, n * sizeof(unsigned), st));
         for (size_t j = 0; j < n; ++j) {
             set_knobs(j);
-            if (t->opts.verify) CU(cudaMemsetAsync(t->opts.y, 0xFF, ybytes, st));
-            CU(cudaEventRecord(ev[2 * j], st));
+            // one untimed launch first: module loading and cold caches never inflate t_verify
             cudaError_t e = fn[j] ? fn[j](ctx) : cudaErrorInvalidDeviceFunction;
-            CU(cudaEventRecord(ev[2 * j + 1], st));
+            if (e == cudaSuccess) {
+                if (t->opts.verify) CU(cudaMemsetAsync(t->opts.y, 0xFF, ybytes, st));
+                CU(cudaEventRecord(ev[2 * j], st));
+                e = fn[j](ctx);
+                CU(cudaEventRecord(ev[2 * j + 1], st));
+            }
             if (e != cudaSuccess) {
                 cudaGetLastError();
                 out[j].status = TUNER_S_LAUNCH_FAIL;
@@ -194,13 +206,21 @@ struct GpuMeasurer : Measurer {
         }
 
         // early cut (SURVEY d.5): rank hopeless candidates by their verify run
+        // and time clearly non-competitive ones (> 1.5x) with 3 repeats instead of R
         std::vector<char> cut(n, 0);
+        std::vector<int> reps(n, R), warm(n, W);
         if (t->opts.early_cut > 0.0) {
             double ref_ns = incumbent;
             for (size_t j = 0; j < n; ++j)
                 if (out[j].status == TUNER_S_OK) ref_ns = std::min(ref_ns, tver[j]);
-            for (size_t j = 0; j < n; ++j)
-                if (out[j].status == TUNER_S_OK && tver[j] > t->opts.early_cut * ref_ns) cut[j] = 1;
+            for (size_t j = 0; j < n; ++j) {
+                if (out[j].status != TUNER_S_OK) continue;
+                if (tver[j] > t->opts.early_cut * ref_ns) cut[j] = 1;
+                else if (tver[j] > kLightFactor * ref_ns) {
+                    reps[j] = std::min(R, 3);
+                    warm[j] = std::min(W, 1);
+                }
+            }
         }
 
         // ---- phase 2: timing
@@ -215,8 +235,13 @@ struct GpuMeasurer : Measurer {
                 double want = 20000.0 / std::max(tver[j], 1.0);
                 num = (int)std::min(100.0, std::max(1.0, std::ceil(want)));
             }
+            // a graph of G <= 8 launches replayed L times per repeat: few nodes to capture
+            // and instantiate on the host, and back-to-back launches on the device
+            const int G = std::min(num, kMaxGraphNodes);
+            const int Lr = (num + G - 1) / G;
+            num = G * Lr;
             number[j] = num;
-            for (int i = 0; i < W; ++i) {
+            for (int i = 0; i < warm[j]; ++i) {
                 cudaError_t e = fn[j](ctx);
                 if (e != cudaSuccess) return cuda_fail(e, "warm-up launch");
             }
@@ -224,7 +249,7 @@ struct GpuMeasurer : Measurer {
             cc.stream = cap;
             set_capturing(true);
             cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
-            for (int i = 0; i < num && e == cudaSuccess; ++i) e = fn[j](cc);
+            for (int i = 0; i < G && e == cudaSuccess; ++i) e = fn[j](cc);
             cudaGraph_t g = nullptr;
             cudaError_t e2 = cudaStreamEndCapture(cap, &g);
             set_capturing(false);
@@ -235,8 +260,8 @@ struct GpuMeasurer : Measurer {
             if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
             const size_t b = tb + j * (size_t)(R + 1);
             CU(cudaEventRecord(ev[b], st));
-            for (int r = 0; r < R; ++r) {
-                CU(cudaGraphLaunch(execs[j], st));
+            for (int r = 0; r < reps[j]; ++r) {
+                for (int l = 0; l < Lr; ++l) CU(cudaGraphLaunch(execs[j], st));
                 count_launches(num);
                 CU(cudaEventRecord(ev[b + r + 1], st));
             }
@@ -256,13 +281,23 @@ struct GpuMeasurer : Measurer {
                 continue;
             }
             const size_t b = tb + j * (size_t)(R + 1);
-            for (int r = 0; r < R; ++r) {
+            const int Rj = reps[j];
+            for (int r = 0; r < Rj; ++r) {
                 float ms = 0.f;
                 CU(cudaEventElapsedTime(&ms, ev[b + r], ev[b + r + 1]));
                 per[r] = (double)ms * 1e6 / number[j];
             }
-            std::sort(per.begin(), per.end());
-            out[j].cost_ns = (R % 2) ? per[R / 2] : 0.5 * (per[R / 2 - 1] + per[R / 2]);
+            // R-M2: trimmed mean (drop the fastest and slowest repeat) for R >= 5, median for
+            // R < 5 -- the device timer ticks in ~1 us steps, so a plain median of 20 us
+            // repeats is quantised to ~5 % and creates artificial ties between neighbours.
+            std::sort(per.begin(), per.begin() + Rj);
+            if (Rj >= 5) {
+                double sum = 0.0;
+                for (int r = 1; r < Rj - 1; ++r) sum += per[r];
+                out[j].cost_ns = sum / (Rj - 2);
+            } else {
+                out[j].cost_ns = (Rj % 2) ? per[Rj / 2] : 0.5 * (per[Rj / 2 - 1] + per[Rj / 2]);
+            }
         }
         return TUNER_OK;
     }
