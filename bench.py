@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--no-bf16-probe", action="store_true",
+                    help="skip the untimed tensor-core probe (DPAnsor on two compute-bound bf16 layers)")
     return ap.parse_args()
 
 
@@ -305,6 +307,27 @@ def main():
     cands = sum(r["candidates"] for r in recs)
     value = cands / (tot_ms / 1e3)
 
+    # tensor-core probe (outside the timed region): 300 samples + Droplet on two compute-bound
+    # bf16 layers of configs[2]/[3], reported against the measured bf16 peak
+    probe = None
+    if dtype == "f32" and not args.no_bf16_probe and world == 1:
+        from synth import BERT, VGG16
+        probe = {"unit": "TFLOP/s", "peak": pk["bf16_tflops"], "bound": "tensor", "layers": []}
+        for L in (VGG16[7], BERT[3]):
+            x, w = layer_tensors(L, 0x5EED)
+            xd = torch.from_numpy(x).to(dev).to(torch.bfloat16)
+            wd = torch.from_numpy(w).to(dev).to(torch.bfloat16)
+            y = torch.empty(out_shape(L), device=dev)
+            tu = Tuner(L["op"], shape_of(L), dtype="bf16", x=xd, w=wd, y=y, seed=0, stream=stream,
+                       early_cut=args.early_cut)
+            tu.sample(args.n_sample)
+            rep = tu.droplet(tu.best().point, args.droplet_budget)
+            tf = layer_flops(L) / rep["best_cost"] / 1e3
+            probe["layers"].append({"layer": L["name"], "best": tu.values(rep["best"]),
+                                    "best_ns": rep["best_cost"], "achieved": tf, "frac": tf / pk["bf16_tflops"]})
+            tu.close()
+            del xd, wd, y
+
     # e2e: host buffers through the public API, H2D + D2H inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -360,7 +383,7 @@ def main():
                                 "max": max(quality) if quality else None,
                                 "within_5pct": sum(q <= 1.05 for q in quality), "layers": len(quality)},
         "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
-        "cpu_baseline": cpu_baseline, "per_layer": recs,
+        "cpu_baseline": cpu_baseline, "bf16_probe": probe, "per_layer": recs,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

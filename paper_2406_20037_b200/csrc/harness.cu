@@ -48,7 +48,7 @@ static tuner_status cuda_fail(cudaError_t e, const char* what) {
 
 // launcher + runtime knobs of a point
 struct RuntimeKnobs {
-    int split = 1, vec = 1, stages = 1;
+    int split = 1, vec = 1, stages = 1, sched = 0;
 };
 static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
     int32_t v[TUNER_MAX_KNOBS];
@@ -64,9 +64,11 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[4]));
         case SK_TC_GEMM_BF16:
             rk.split = v[4];
+            rk.sched = v[5];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], 0));
         case SK_TC_IGEMM_CONV_BF16:
             rk.split = v[4];
+            rk.sched = v[6];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[5]));
         default: return nullptr;
     }
@@ -162,11 +164,12 @@ struct GpuMeasurer : Measurer {
         std::vector<char> launched(n, 0);
         for (size_t j = 0; j < n; ++j) fn[j] = resolve(t, pts[j], rk[j]);
         const size_t ybytes = (size_t)t->info.y_elems * sizeof(float);
-        LaunchCtx ctx{&t->info, t->opts.x, t->opts.w, t->opts.y, 1, 1, 1, st, nsm};
+        LaunchCtx ctx{&t->info, t->opts.x, t->opts.w, t->opts.y, 1, 1, 1, 0, st, nsm};
         auto set_knobs = [&](size_t j) {
             ctx.split = rk[j].split;
             ctx.vec = rk[j].vec;
             ctx.stages = rk[j].stages;
+            ctx.sched = rk[j].sched;
         };
 
         // ---- phase 1: verification run (also the first, untimed-for-cost launch)
@@ -320,7 +323,7 @@ tuner_status gpu_kernel_run(const Tuner* t, const Pt& p, const tuner_buffers* bu
     int nsm = 148, dev = 0;
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    LaunchCtx ctx{&t->info, buf->x, buf->w, buf->y, rk.split, rk.vec, rk.stages, (cudaStream_t)stream, nsm};
+    LaunchCtx ctx{&t->info, buf->x, buf->w, buf->y, rk.split, rk.vec, rk.stages, rk.sched, (cudaStream_t)stream, nsm};
     CU(fn(ctx));
     return TUNER_OK;
 }

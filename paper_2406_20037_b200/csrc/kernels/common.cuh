@@ -17,6 +17,7 @@ struct LaunchCtx {
     int split;             // runtime SPLIT_K knob
     int vec;               // runtime VEC knob (SIMT)
     int stages;            // runtime STAGES knob (SIMT)
+    int sched;             // runtime SCHED knob (tcgen05: 0 tiles, 1 stream-K)
     cudaStream_t stream;
     int num_sms;
 };

@@ -38,6 +38,8 @@
 
 namespace db200 {
 
+static constexpr int kStreamKSlots = 1024;  // (group, CTA) workspace slots of a stream-K launch
+
 template <int BN, int BK, int STAGES, int CG>
 struct TcCfg {
     static constexpr int BM = 128;  // rows of A per CTA
@@ -55,7 +57,11 @@ struct TcParams {
     int kblocks, split;
     int m_tiles;                  // 128-row sub-tiles per batch (conv: images x pixel tiles)
     int mp_tiles, n_tiles, batch;  // tiles of the CTA group (CG sub-tiles each)
-    int units;                    // batch * mp_tiles * n_tiles * split
+    int units;                    // SCHED 0: batch * mp_tiles * n_tiles * split
+    int sched;                    // 0 = tiles (+ split-K), 1 = stream-K
+    long long total_iters;        // SCHED 1: tiles * kblocks
+    unsigned* flags;              // SCHED 1: per workspace slot (group x CTA): 1 = partial parked
+    float* ws;                    // SCHED 1: [slot][128][BN] partial accumulators of tails
     float* C;
     // implicit GEMM
     int P, Q, S, CB;  // CB = channel blocks of BK per tap
@@ -63,23 +69,64 @@ struct TcParams {
     int tiles_p, tiles_q;
 };
 
-struct Unit {
+// epilogue modes of a segment: plain store; split-K reduction into a zeroed Y;
+// stream-K head (wait for the tile's tails, add their partials, store); stream-K
+// tail (park the partial in the group's workspace slot and signal)
+enum : int { EPI_STORE = 0, EPI_RED = 1, EPI_HEAD = 2, EPI_TAIL = 3 };
+
+struct Seg {
+    int tile;                  // linear tile index (m fastest), SCHED 1 flag index base
     int bz, mt, nt, kb0, nkb;  // mt = index of the CTA group's tile
+    int mode;
+    int ntails;                // SCHED 1: segments of this tile after its head
 };
 
-__device__ __forceinline__ Unit decode_unit(const TcParams& p, int u) {
-    Unit w;
-    const int kz = u % p.split;
-    int t = u / p.split;
-    w.mt = t % p.mp_tiles;  // m fastest: concurrent CTAs share the B (weight) tile in L2
-    t /= p.mp_tiles;
-    w.nt = t % p.n_tiles;
-    w.bz = t / p.n_tiles;
-    // balanced k slices: every slice is non-empty when split <= kblocks (static validity)
-    w.kb0 = (int)((long long)kz * p.kblocks / p.split);
-    w.nkb = (int)((long long)(kz + 1) * p.kblocks / p.split) - w.kb0;
-    return w;
-}
+// Walks the segments (tile, k range) of one CTA group.  SCHED 0: units u = g, g+G, ...
+// (tile x split-K slice, balanced slices).  SCHED 1 (stream-K): the contiguous share
+// [g*T/G, (g+1)*T/G) of all T = tiles * kblocks iterations, cut at tile boundaries.
+struct SegIter {
+    long long cur, end;
+    int u;
+    __device__ SegIter(const TcParams& p, int g, int G) {
+        u = g;
+        cur = (long long)g * p.total_iters / G;
+        end = (long long)(g + 1) * p.total_iters / G;
+    }
+    __device__ bool next(const TcParams& p, int G, Seg& s) {
+        int t;
+        if (p.sched == 0) {
+            if (u >= p.units) return false;
+            const int kz = u % p.split;
+            t = u / p.split;
+            s.kb0 = (int)((long long)kz * p.kblocks / p.split);  // non-empty when split <= kblocks
+            s.nkb = (int)((long long)(kz + 1) * p.kblocks / p.split) - s.kb0;
+            s.mode = p.split > 1 ? EPI_RED : EPI_STORE;
+            u += G;
+        } else {
+            if (cur >= end) return false;
+            t = (int)(cur / p.kblocks);
+            s.kb0 = (int)(cur - (long long)t * p.kblocks);
+            const long long left = end - cur;
+            s.nkb = (int)((long long)(p.kblocks - s.kb0) < left ? (p.kblocks - s.kb0) : left);
+            const bool head = s.kb0 == 0, whole = head && s.nkb == p.kblocks;
+            // a head that is not the whole tile is the LAST segment of its group's range and
+            // a tail is the FIRST one: heads wait for tails finished early -- no chain
+            s.mode = whole ? EPI_STORE : (head ? EPI_HEAD : EPI_TAIL);
+            // groups sharing this tile: g(i) = ceil((i+1) G / T) - 1 owns iteration i
+            const long long T = p.total_iters, i0 = (long long)t * p.kblocks, i1 = i0 + p.kblocks - 1;
+            s.ntails = (int)(((i1 + 1) * G + T - 1) / T - ((i0 + 1) * G + T - 1) / T);
+            cur += s.nkb;
+        }
+        s.tile = t;
+        s.mt = t % p.mp_tiles;  // m fastest: concurrent CTAs share the B (weight) tile in L2
+        t /= p.mp_tiles;
+        s.nt = t % p.n_tiles;
+        s.bz = t / p.n_tiles;
+        return true;
+    }
+};
+
+__device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 
 template <int BN, int BK, int STAGES, int TQ, int CG>
 __global__ void __launch_bounds__(192, 1)
@@ -126,13 +173,14 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t tmem = *tmem_slot;
 
     // this CTA's 128-row sub-tile of the group's tile
-    auto sub_tile = [&](const Unit& w) { return w.mt * CG + (int)rank; };
+    auto sub_tile = [&](const Seg& w) { return w.mt * CG + (int)rank; };
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer: one continuous ring across units
             int it = 0;
-            for (int u = group; u < p.units; u += ngroups) {
-                const Unit w = decode_unit(p, u);
+            SegIter si(p, group, ngroups);
+            Seg w;
+            while (si.next(p, ngroups, w)) {
                 const int mt = sub_tile(w);
                 int img = w.bz, p0 = 0, q0 = 0;
                 if constexpr (CONV) {
@@ -189,8 +237,9 @@ __global__ void __launch_bounds__(192, 1)
         if (lane == 0 && rank == 0) {  // ---- MMA issuer (the leader CTA of a pair)
             constexpr uint32_t idesc = tc::idesc_bf16(BM * CG, BN);
             int it = 0, j = 0;
-            for (int u = group; u < p.units; u += ngroups, ++j) {
-                const Unit w = decode_unit(p, u);
+            SegIter si(p, group, ngroups);
+            Seg w;
+            for (; si.next(p, ngroups, w); ++j) {
                 const int a = j & 1;
                 tc::mbar_wait(tc::smem_u32(&acc_empty[a]), ((uint32_t)(j >> 1) & 1u) ^ 1u);
                 tc::tc_fence_after();
@@ -223,8 +272,9 @@ __global__ void __launch_bounds__(192, 1)
         const int trow = q * 32 + lane;  // row of the 128-row sub-tile held by this thread
         const bool vec_ok = (p.N % 4) == 0;
         int j = 0;
-        for (int u = group; u < p.units; u += ngroups, ++j) {
-            const Unit w = decode_unit(p, u);
+        SegIter si(p, group, ngroups);
+        Seg w;
+        for (; si.next(p, ngroups, w); ++j) {
             const int mt = sub_tile(w);
             const int a = j & 1;
             bool row_ok = mt < p.m_tiles;
@@ -243,8 +293,25 @@ __global__ void __launch_bounds__(192, 1)
             }
             tc::mbar_wait(tc::smem_u32(&acc_full[a]), (uint32_t)(j >> 1) & 1u);
             tc::tc_fence_after();
-            float* crow = p.C + orow * p.N;
-            const int n0 = w.nt * BN;
+            const int slot = group * CG + (int)rank;  // this group's workspace slot (stream-K)
+            if (w.mode == EPI_HEAD) {  // wait until every tail of this tile parked its partial
+                if (warp == 2 && lane == 0) {
+                    for (int tl = 1; tl <= w.ntails; ++tl) {
+                        const unsigned* f = p.flags + (slot + tl * CG);
+                        unsigned v;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                        } while (v == 0u);
+                    }
+                }
+                epi_bar(1);
+            }
+            const bool red = w.mode == EPI_RED;
+            float* crow = w.mode == EPI_TAIL ? p.ws + ((long long)slot * 128 + trow) * BN  // parked partial
+                                             : p.C + orow * p.N;
+            const int n0 = w.mode == EPI_TAIL ? 0 : w.nt * BN;
+            const bool live = w.mode == EPI_TAIL ? true : row_ok;
+            const int ncols = w.mode == EPI_TAIL ? BN : p.N;
             constexpr int CH = BN < 64 ? BN : 64;  // columns per TMEM drain: several loads, one wait
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += CH) {
@@ -256,20 +323,33 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                 for (int g = 0; g < CH / 16; ++g) {
                     const int n = n0 + c0 + g * 16;
-                    if (!row_ok || n >= p.N) continue;
-                    if (vec_ok && n + 16 <= p.N) {
+                    if (!live || n >= ncols) continue;
+                    if (w.mode == EPI_HEAD) {  // add the tails' partials (same rows, same columns)
+                        for (int tl = 1; tl <= w.ntails; ++tl) {
+                            const float* pp = p.ws + ((long long)(slot + tl * CG) * 128 + trow) * BN + c0 + g * 16;
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                const float4 x = __ldcg(reinterpret_cast<const float4*>(pp) + v);
+                                r[g][4 * v] = __float_as_uint(__uint_as_float(r[g][4 * v]) + x.x);
+                                r[g][4 * v + 1] = __float_as_uint(__uint_as_float(r[g][4 * v + 1]) + x.y);
+                                r[g][4 * v + 2] = __float_as_uint(__uint_as_float(r[g][4 * v + 2]) + x.z);
+                                r[g][4 * v + 3] = __float_as_uint(__uint_as_float(r[g][4 * v + 3]) + x.w);
+                            }
+                        }
+                    }
+                    if ((vec_ok || w.mode == EPI_TAIL) && n + 16 <= ncols) {
 #pragma unroll
                         for (int v = 0; v < 4; ++v) {
                             float4 f = make_float4(__uint_as_float(r[g][4 * v]), __uint_as_float(r[g][4 * v + 1]),
                                                    __uint_as_float(r[g][4 * v + 2]), __uint_as_float(r[g][4 * v + 3]));
-                            if (p.split > 1) tc::red_add_v4(crow + n + 4 * v, f.x, f.y, f.z, f.w);
+                            if (red) tc::red_add_v4(crow + n + 4 * v, f.x, f.y, f.z, f.w);
                             else *reinterpret_cast<float4*>(crow + n + 4 * v) = f;
                         }
                     } else {
 #pragma unroll
                         for (int jj = 0; jj < 16; ++jj) {
-                            if (n + jj < p.N) {
-                                if (p.split > 1) atomicAdd(crow + n + jj, __uint_as_float(r[g][jj]));
+                            if (n + jj < ncols) {
+                                if (red) atomicAdd(crow + n + jj, __uint_as_float(r[g][jj]));
                                 else crow[n + jj] = __uint_as_float(r[g][jj]);
                             }
                         }
@@ -281,6 +361,18 @@ __global__ void __launch_bounds__(192, 1)
             if (lane == 0) {  // this warp's accumulator lanes are drained
                 if constexpr (CG == 2) tc::mbar_arrive_remote(tc::smem_u32(&acc_empty[a]), 0);
                 else tc::mbar_arrive(tc::smem_u32(&acc_empty[a]));
+            }
+            if (w.mode == EPI_TAIL) {  // publish the parked partial (flag = 1)
+                epi_bar(2);
+                if (warp == 2 && lane == 0) {
+                    __threadfence();
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.flags + slot), "r"(1u) : "memory");
+                }
+            } else if (w.mode == EPI_HEAD) {  // partials consumed: re-arm the tails' flags (0)
+                epi_bar(2);
+                if (warp == 2 && lane == 0) {
+                    for (int tl = 1; tl <= w.ntails; ++tl) p.flags[slot + tl * CG] = 0u;
+                }
             }
         }
     }
@@ -319,6 +411,31 @@ static bool encode(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* 
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+// stream-K scratch, per device, allocated once (outside graph capture: the first
+// launch of a schedule is never captured): kStreamKSlots flags, zeroed once and
+// left at 0 by every launch (heads re-arm their tails' flags), and one
+// 128 x 256 fp32 partial-accumulator slot per (group, CTA)
+static bool stream_k_scratch(unsigned** flags, float** ws) {
+    static unsigned* fl[64] = {};
+    static float* w[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    dev &= 63;
+    if (!fl[dev]) {
+        unsigned* f = nullptr;
+        float* b = nullptr;
+        if (cudaMalloc(&f, kStreamKSlots * sizeof(unsigned)) != cudaSuccess) return false;
+        if (cudaMemset(f, 0, kStreamKSlots * sizeof(unsigned)) != cudaSuccess) return false;
+        if (cudaMalloc(&b, (size_t)kStreamKSlots * 128 * 256 * sizeof(float)) != cudaSuccess) return false;
+        if (cudaDeviceSynchronize() != cudaSuccess) return false;
+        fl[dev] = f;
+        w[dev] = b;
+    }
+    *flags = fl[dev];
+    *ws = w[dev];
+    return true;
 }
 
 // 3-D K-major operand [batch][rows][K] -> box {64, box_rows, 1}
@@ -380,20 +497,30 @@ cudaError_t tc_launch(const LaunchCtx& c) {
         p.batch = (int)s.batch;
     }
     p.mp_tiles = (p.m_tiles + CG - 1) / CG;
-    const long long units = (long long)p.batch * p.mp_tiles * p.n_tiles * c.split;
+    const long long tiles = (long long)p.batch * p.mp_tiles * p.n_tiles;
+    const long long units = tiles * c.split;
     if (units >= (1ll << 31)) return cudaErrorInvalidValue;
     p.units = (int)units;
+    p.sched = c.sched;
+    p.total_iters = tiles * p.kblocks;
     if (c.split > 1) {
         cudaError_t e = cudaMemsetAsync(c.y, 0, (size_t)s.y_elems * sizeof(float), c.stream);
         if (e != cudaSuccess) return e;
     }
-    // persistent grid: CTA groups = SMs / CG x resident slots (shared memory and TMEM limited)
+    // persistent grid: CTA groups = SMs / CG x resident slots (shared memory and TMEM limited);
+    // every group must be co-resident for the stream-K flag protocol
     int per_sm = (int)((228 * 1024) / (Cfg::SMEM + 1024));
     per_sm = per_sm < 1 ? 1 : per_sm;
     const int tmem_per_sm = (int)(512 / Cfg::TMEM_COLS);
     per_sm = per_sm < tmem_per_sm ? per_sm : tmem_per_sm;
     long long groups = (long long)(c.num_sms / CG) * per_sm;
-    if (groups > units) groups = units;
+    if (c.sched == 1) {
+        if (!stream_k_scratch(&p.flags, &p.ws)) return cudaErrorMemoryAllocation;
+        if (groups > p.total_iters) groups = p.total_iters;
+        if (groups * CG > kStreamKSlots) groups = kStreamKSlots / CG;
+    } else if (groups > units) {
+        groups = units;
+    }
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)(groups * CG));
