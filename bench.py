@@ -73,6 +73,24 @@ def peaks():
             "source": "MEASURED_PEAKS.json" if mp else "B200_PROFILING.md fallback"}
 
 
+def traffic_evidence():
+    """DRAM traffic of the best r18.l1.3x3 schedule from the committed ncu --set full capture
+    (profiles/r1_ncu_simt_r18l1.raw.csv) next to that layer's algorithmic bytes."""
+    import csv
+    path = os.path.join(ROOT, "profiles", "r1_ncu_simt_r18l1.raw.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+        d = {h: (v, u) for h, u, v in zip(rows[0], rows[1], rows[2])}
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        by = sum(float(d[m][0].replace(",", "")) * scale.get(d[m][1], 1)
+                 for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    except Exception:
+        return None
+    algo = 4 * (56 * 56 * 64 + 64 * 9 * 64 + 56 * 56 * 64)  # X + W + Y, fp32
+    return {"capture": "profiles/r1_ncu_simt_r18l1.raw.csv", "layer": "r18.l1.3x3", "dram_bytes": by,
+            "algorithmic_bytes": algo, "ratio": by / algo}
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -365,6 +383,9 @@ def main():
         roofline = {"bound": "tensor", "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst) = {peak}"}
     roofline.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
                      "kernel": "best 300+Droplet schedule per timed layer; sum F / sum median CUDA-event time"})
+    ev = traffic_evidence() if dtype == "f32" else None
+    if ev:
+        roofline["traffic_evidence"] = ev
     dp_wall = sum(r["dp_wall_s"] for r in tuned)
     bl_wall = sum(r["bl_wall_s"] for r in tuned)
     quality = [r["dp_best_ns"] / r["bl_best_ns"] for r in tuned if r["bl_best_ns"] < math.inf]
