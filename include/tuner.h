@@ -195,6 +195,16 @@ tuner_status tuner_point_valid(const tuner_t* t, const tuner_point* pt, int32_t*
  * *n_out = number actually drawn (< n only if 64*n draws were exhausted). */
 tuner_status tuner_sample(tuner_t* t, int32_t n, tuner_result* out, int32_t* n_out);
 
+/* Ansor-style evolutionary exploration (reading R-E1; the learned cost
+ * model is out of scope, so every child is measured): generation 0 is
+ * tuner_sample's draw of min(pop, n) points; each later generation breeds up to
+ * min(pop, n - used) new valid, unmeasured children from the `elite` best
+ * measured points by uniform crossover (same sketch) and one resampled knob.
+ * out: caller array of n; *n_out = points measured (< n if the space runs dry).
+ * EINVAL if pop < 1 or elite < 1. */
+tuner_status tuner_evolve(tuner_t* t, int32_t n, int32_t pop, int32_t elite, tuner_result* out,
+                          int32_t* n_out);
+
 /* Measure an explicit list of points (e.g. exhaustive grid).
  * Already-measured points are returned from the memo and not re-measured. */
 tuner_status tuner_measure(tuner_t* t, const tuner_point* pts, int32_t n, tuner_result* out);

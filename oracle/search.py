@@ -138,6 +138,7 @@ class OracleTuner:
         self.history: List[Tuple[Point, float]] = []
         self.memo: Dict[Point, float] = {}
         self.batches: List[List[Point]] = []
+        self.generations: List[Tuple[List[Point], List[Point]]] = []  # evolve(): (parents, children)
 
     # one measured batch, in batch order (sharding changes nothing, R-M1)
     def measure(self, batch: List[Point]) -> None:
@@ -168,6 +169,66 @@ class OracleTuner:
         for i in range(0, len(pts), max_batch):
             self.measure(pts[i:i + max_batch])
         return [(p, self.memo[p]) for p in pts]
+
+    # ------------------------------------------------------------------ evolutionary exploration
+    def evolve(self, n: int, pop: int = 64, elite: int = 16, max_batch: int = 512) -> List[Tuple[Point, float]]:
+        """Ansor-style evolution of the annotated population (R-E1), without
+        the learned cost model: every child is measured.
+
+        Generation 0 is ``draw(min(pop, n))`` (the sampler, R-S1).  Each later generation
+        takes the ``elite`` best measured points of the whole history (cost, then
+        measurement order; finite costs only) as parents and produces up to
+        min(pop, n - used) new children, each:
+          a = parents[uniform(E)]; op = uniform(2)
+          op == 1: b = parents[uniform(E)]; if b is of a's sketch, for every knob d
+                   child[d] = (a[d], b[d])[uniform(2)], else child = a
+          op == 0: child = a
+          mutation: d = uniform(nknobs); child[d] = uniform(card_d)
+        A child is kept iff valid, unmeasured and new in this generation; at most 64*pop
+        attempts per generation; an empty generation ends the run.
+        """
+        out: List[Point] = []
+        first = self.draw(min(pop, n))
+        for i in range(0, len(first), max_batch):
+            self.measure(first[i:i + max_batch])
+        out += first
+        used = len(first)
+        while used < n:
+            ranked = sorted(((c, k, p) for k, (p, c) in enumerate(self.history) if math.isfinite(c)))
+            parents = [p for _, _, p in ranked[:elite]]
+            if not parents:
+                break
+            want = min(pop, n - used)
+            children: List[Point] = []
+            taken = set()
+            attempts = 0
+            while len(children) < want and attempts < 64 * pop:
+                attempts += 1
+                a = parents[self.rng.uniform(len(parents))]
+                child = list(a[1])
+                if self.rng.uniform(2) == 1:
+                    b = parents[self.rng.uniform(len(parents))]
+                    if b[0] == a[0]:
+                        for d in range(len(child)):
+                            if self.rng.uniform(2) == 1:
+                                child[d] = b[1][d]
+                cards = self.space.cards(a[0])
+                if cards:
+                    d = self.rng.uniform(len(cards))
+                    child[d] = self.rng.uniform(cards[d])
+                c = (a[0], tuple(child))
+                if not self.valid(c) or c in self.memo or c in taken:
+                    continue
+                taken.add(c)
+                children.append(c)
+            if not children:
+                break
+            self.generations.append((list(parents), list(children)))
+            for i in range(0, len(children), max_batch):
+                self.measure(children[i:i + max_batch])
+            out += children
+            used += len(children)
+        return [(p, self.memo[p]) for p in out]
 
     def best(self) -> Tuple[Point, float]:
         """First argmin of cost over history, in measurement order (R-B1)."""

@@ -137,6 +137,8 @@ struct Tuner {
 
     tuner_status measure_batch(const std::vector<Pt>& batch);
     tuner_status draw(int32_t n, std::vector<Pt>& out);
+    tuner_status measure_chunked(const std::vector<Pt>& pts);
+    tuner_status evolve(int32_t n, int32_t pop, int32_t elite, std::vector<Pt>& out);
     tuner_status droplet(const Pt& start, int32_t budget, std::vector<Pt>& traj,
                          tuner_droplet_report& rep);
 };

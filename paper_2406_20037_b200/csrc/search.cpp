@@ -5,6 +5,7 @@
 // Paper: Def. 2.1, Example 2.3, neighbourhood
 // (P:290-294), Droplet Search, combined approach,
 // Droplet cap of 100 trials.  Readings R-xx: DESIGN.md §3.
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <limits>
@@ -172,6 +173,74 @@ tuner_status Tuner::draw(int32_t n, std::vector<Pt>& out) {
         if (memo.count(id) || taken.count(id)) continue;
         taken.insert(id);
         out.push_back(p);
+    }
+    return TUNER_OK;
+}
+
+tuner_status Tuner::measure_chunked(const std::vector<Pt>& pts) {
+    for (size_t i = 0; i < pts.size(); i += (size_t)opts.max_batch) {
+        size_t e = std::min(pts.size(), i + (size_t)opts.max_batch);
+        tuner_status st = measure_batch(std::vector<Pt>(pts.begin() + i, pts.begin() + e));
+        if (st != TUNER_OK) return st;
+    }
+    return TUNER_OK;
+}
+
+// ---------------------------------------------------------------- evolutionary exploration
+// Ansor's evolution of annotated sketches without the learned cost
+// model (every child is measured), R-E1: generation 0 = the sampler; then each
+// generation draws children from the `elite` best measured points (cost, then
+// measurement order): a = parent[u(E)]; if u(2) == 1, b = parent[u(E)] and, when b
+// has a's sketch, each knob takes b's index if u(2) == 1; then one knob d = u(nknobs)
+// is resampled, child[d] = u(card_d).  Children must be valid, unmeasured and new in
+// their generation (<= 64*pop attempts); an empty generation ends the run.
+tuner_status Tuner::evolve(int32_t n, int32_t pop, int32_t elite, std::vector<Pt>& out) {
+    out.clear();
+    std::vector<Pt> gen;
+    draw(std::min(pop, n), gen);
+    tuner_status st = measure_chunked(gen);
+    if (st != TUNER_OK) return st;
+    out = gen;
+    int32_t used = (int32_t)gen.size();
+    while (used < n) {
+        std::vector<std::pair<double, size_t>> ranked;
+        for (size_t i = 0; i < history.size(); ++i)
+            if (std::isfinite(history[i].cost_ns)) ranked.emplace_back(history[i].cost_ns, i);
+        std::sort(ranked.begin(), ranked.end());
+        std::vector<Pt> parents;
+        for (size_t i = 0; i < ranked.size() && (int32_t)parents.size() < elite; ++i) {
+            tuner_status s2;
+            parents.push_back(from_public(history[ranked[i].second].pt, s2));
+        }
+        if (parents.empty()) break;
+        const int32_t want = std::min(pop, n - used);
+        const uint32_t E = (uint32_t)parents.size();
+        gen.clear();
+        std::unordered_set<uint64_t> taken;
+        for (int64_t attempts = 0; (int32_t)gen.size() < want && attempts < 64ll * pop; ++attempts) {
+            const Pt& a = parents[rng.uniform(E)];
+            Pt child = a;
+            if (rng.uniform(2) == 1) {
+                const Pt& b = parents[rng.uniform(E)];
+                if (b.pos == a.pos)
+                    for (int d = 0; d < child.n; ++d)
+                        if (rng.uniform(2) == 1) child.idx[d] = b.idx[d];
+            }
+            const SketchSpace& sp = spaces[a.pos];
+            if (sp.nknobs() > 0) {
+                const int d = (int)rng.uniform((uint32_t)sp.nknobs());
+                child.idx[d] = (int32_t)rng.uniform((uint32_t)sp.values[d].size());
+            }
+            if (!valid(child)) continue;
+            const uint64_t id = linear(child);
+            if (memo.count(id) || taken.count(id)) continue;
+            taken.insert(id);
+            gen.push_back(child);
+        }
+        if (gen.empty()) break;
+        if ((st = measure_chunked(gen)) != TUNER_OK) return st;
+        out.insert(out.end(), gen.begin(), gen.end());
+        used += (int32_t)gen.size();
     }
     return TUNER_OK;
 }
@@ -459,6 +528,19 @@ extern "C" tuner_status tuner_sample(tuner_t* t, int32_t n, tuner_result* out, i
         tuner_status st = t->measure_batch(b);
         if (st != TUNER_OK) return after(t, st);
     }
+    for (size_t i = 0; i < pts.size(); ++i) fill_sample(t, pts[i], &out[i]);
+    *n_out = (int32_t)pts.size();
+    return TUNER_OK;
+}
+
+extern "C" tuner_status tuner_evolve(tuner_t* t, int32_t n, int32_t pop, int32_t elite, tuner_result* out,
+                                     int32_t* n_out) {
+    CHECK_HANDLE(t);
+    if (n < 0 || pop < 1 || elite < 1 || (n > 0 && !out) || !n_out) return fail(TUNER_EINVAL, "bad arguments");
+    *n_out = 0;
+    std::vector<Pt> pts;
+    tuner_status st = t->evolve(n, pop, elite, pts);
+    if (st != TUNER_OK) return after(t, st);
     for (size_t i = 0; i < pts.size(); ++i) fill_sample(t, pts[i], &out[i]);
     *n_out = (int32_t)pts.size();
     return TUNER_OK;

@@ -196,6 +196,13 @@ class Tuner:
         L.check(L.lib().tuner_sample(self._h, n, out, C.byref(got)))
         return [_sample(out[i]) for i in range(got.value)]
 
+    def evolve(self, n: int, pop: int = 64, elite: int = 16) -> List[Sample]:
+        """Ansor-style evolutionary exploration (tuner_evolve)."""
+        out = (L.Result * max(1, n))()
+        got = C.c_int32()
+        L.check(L.lib().tuner_evolve(self._h, n, pop, elite, out, C.byref(got)))
+        return [_sample(out[i]) for i in range(got.value)]
+
     def measure(self, points: Sequence[PointT]) -> List[Sample]:
         n = len(points)
         pts = (L.Point * max(1, n))(*[_point(p) for p in points])
