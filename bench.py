@@ -39,6 +39,8 @@ def parse():
                     choices=["resnet", "resnet18", "resnet50", "vgg16", "alexnet", "vgg_alexnet", "bert", "bert1",
                              "config1"])
     ap.add_argument("--n-sample", type=int, default=300)
+    ap.add_argument("--explore", default="evolve", choices=["evolve", "random"],
+                    help="exploration phase of DPAnsor: Ansor-style evolution (default) or uniform sampling")
     ap.add_argument("--droplet-budget", type=int, default=100)
     ap.add_argument("--baseline", type=int, default=10000)
     ap.add_argument("--early-cut", type=float, default=4.0)
@@ -255,7 +257,7 @@ def main():
         t0 = time.perf_counter()
         tu = Tuner(L["op"], shape_of(L), dtype=dtype, x=xd, w=wd, y=y, seed=seed, group=group, stream=stream,
                    early_cut=args.early_cut)
-        smp = tu.sample(args.n_sample)
+        smp = tu.evolve(args.n_sample) if args.explore == "evolve" else tu.sample(args.n_sample)
         if not smp:  # no compiled sketch covers this layer (e.g. bf16 TMA needs C % 8 == 0)
             tu.close()
             rec.update(skipped="no statically valid schedule", candidates=0, launches=0, collectives=0)
