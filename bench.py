@@ -246,6 +246,16 @@ def main():
             return {k: L[k] for k in ("N", "C", "H", "W", "K", "R", "S", "stride", "pad", "dil")}
         return {k: L[k] for k in ("b", "m", "n", "k") if k in L}
 
+    from paper_2406_20037_b200 import sketch_space
+
+    def spaces_of(L):
+        # sketch rule (Ansor's rules are hardware-dependent): a bf16 conv is tuned
+        # on the tcgen05 sketch when TMA can address it (C % 8 == 0), else on the SIMT one
+        if dtype == "bf16" and L["op"] == "conv2d":
+            sk = 3 if L["C"] % 8 == 0 else 4
+            return [(sk, sketch_space(sk))]
+        return None
+
     def tune_layer(li, seed, e2e=False, pinned=None):
         L = layers[li]
         xd, wd, y = bufs[li][:3]
@@ -255,8 +265,8 @@ def main():
         rec = {"layer": L["name"], "gflop": layer_flops(L) / 1e9}
         # DPAnsor: sample N, best-of-N, Droplet to convergence (<= 100 trials)
         t0 = time.perf_counter()
-        tu = Tuner(L["op"], shape_of(L), dtype=dtype, x=xd, w=wd, y=y, seed=seed, group=group, stream=stream,
-                   early_cut=args.early_cut)
+        tu = Tuner(L["op"], shape_of(L), dtype=dtype, spaces=spaces_of(L), x=xd, w=wd, y=y, seed=seed, group=group,
+                   stream=stream, early_cut=args.early_cut)
         smp = tu.evolve(args.n_sample) if args.explore == "evolve" else tu.sample(args.n_sample)
         if not smp:  # no compiled sketch covers this layer (e.g. bf16 TMA needs C % 8 == 0)
             tu.close()
@@ -271,8 +281,8 @@ def main():
                    dp_wall_s=t1 - t0, dp_candidates=st["candidates"], launches=st["kernel_launches"],
                    collectives=st["collectives"], wrong=sum(s.status != "ok" for s in tu.history()))
         # the 10,000-trial random baseline on the same harness (fresh history, other seed)
-        bl = Tuner(L["op"], shape_of(L), dtype=dtype, x=xd, w=wd, y=y, seed=seed + 7919, group=group, stream=stream,
-                   early_cut=args.early_cut)
+        bl = Tuner(L["op"], shape_of(L), dtype=dtype, spaces=spaces_of(L), x=xd, w=wd, y=y, seed=seed + 7919,
+                   group=group, stream=stream, early_cut=args.early_cut)
         bl.sample(args.baseline) if args.baseline > 0 else None
         t2 = time.perf_counter()
         bst = bl.stats()

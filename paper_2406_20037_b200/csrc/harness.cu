@@ -58,6 +58,7 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
     switch (sk) {
         case SK_SIMT_GEMM_F32:
         case SK_SIMT_IGEMM_CONV_F32:
+        case SK_SIMT_IGEMM_CONV_BF16:
             rk.vec = v[5];
             rk.stages = v[6];
             rk.split = v[7];

@@ -17,13 +17,15 @@
 //
 // FP32 on the CUDA cores (north_star: "The fp32 SIMT variants stay on CUDA cores").
 #pragma once
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace db200 {
 
 struct SimtParams {
-    const float* __restrict__ A;
-    const float* __restrict__ B;
+    const void* __restrict__ A;  // TIn (float or bf16)
+    const void* __restrict__ B;
     float* __restrict__ C;
     int M, N, K;
     long long sA, sB, sC;  // batch strides
@@ -54,6 +56,16 @@ constexpr bool simt_static_ok(int BM, int BN, int BK, int TT) {
            4 * (cdiv_c(BM * (BK / 4), (BM / TT) * (BN / TT)) + cdiv_c(BN * (BK / 4), (BM / TT) * (BN / TT))) <= 64;
 }
 
+// Global loads of the input element type, widened to fp32 for the CUDA-core FMAs.
+__device__ __forceinline__ float ld1(const float* p) { return __ldg(p); }
+__device__ __forceinline__ float ld1(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {  // 4 x bf16 = one 64-bit load
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+    return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                       __uint_as_float(u.y & 0xFFFF0000u));
+}
+
 // Row r of a thread's TT-row register tile -> row inside the block tile.
 // TT <= 4: contiguous; TT = 8: two 4-row groups BM/2 apart (conflict-free LDS.128).
 template <int BMN, int TT>
@@ -75,7 +87,7 @@ __device__ __forceinline__ RSC rsc_advance(RSC b, int add, int Cin, int S) {
     return b;
 }
 
-template <int BM, int BN, int BK, int TT, int UNROLL, bool CONV>
+template <int BM, int BN, int BK, int TT, int UNROLL, bool CONV, typename TIn>
 __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
     simt_gemm_f32_kernel(const SimtParams p) {
     using Cfg = SimtCfg<BM, BN, BK, TT>;
@@ -95,8 +107,8 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
     const int kt_end = min(p.ktiles, kt_begin + p.kt_per_split);
     if (kt_begin >= kt_end) return;
 
-    const float* __restrict__ A = p.A + (CONV ? 0 : bz * p.sA);
-    const float* __restrict__ B = p.B + bz * p.sB;
+    const TIn* __restrict__ A = (const TIn*)p.A + (CONV ? 0 : bz * p.sA);
+    const TIn* __restrict__ B = (const TIn*)p.B + bz * p.sB;
     float* __restrict__ C = p.C + bz * p.sC;
 
     if constexpr (CONV) {
@@ -135,9 +147,9 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
             const int h = rowinfo[BM + row] + rsc.r * p.dh;
             const int w = rowinfo[2 * BM + row] + rsc.s * p.dw;
             if ((unsigned)h >= (unsigned)p.H || (unsigned)w >= (unsigned)p.W) return 0.f;
-            return __ldg(A + rowinfo[row] + (h * p.W + w) * p.Cin + rsc.c);
+            return ld1(A + rowinfo[row] + (h * p.W + w) * p.Cin + rsc.c);
         } else {
-            return __ldg(A + (long long)(m0 + row) * p.K + kk);
+            return ld1(A + (long long)(m0 + row) * p.K + kk);
         }
     };
 
@@ -165,10 +177,9 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
                             const int h = rowinfo[BM + row] + rsc.r * p.dh;
                             const int w = rowinfo[2 * BM + row] + rsc.s * p.dw;
                             if ((unsigned)h < (unsigned)p.H && (unsigned)w < (unsigned)p.W)
-                                v = __ldg(reinterpret_cast<const float4*>(A + rowinfo[row] + (h * p.W + w) * p.Cin +
-                                                                          rsc.c));
+                                v = ld4(A + rowinfo[row] + (h * p.W + w) * p.Cin + rsc.c);
                         } else {
-                            v = __ldg(reinterpret_cast<const float4*>(A + (long long)(m0 + row) * p.K + kk));
+                            v = ld4(A + (long long)(m0 + row) * p.K + kk);
                         }
                     }
                 } else {  // VEC = 1: four scalar loads
@@ -190,14 +201,14 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             const int kk = k0 + kl;
             if (e < BN * KV && n0 + row < p.N) {
-                const float* bp = B + (long long)(n0 + row) * p.K + kk;
+                const TIn* bp = B + (long long)(n0 + row) * p.K + kk;
                 if (p.vec4) {
-                    if (kk < p.K) v = __ldg(reinterpret_cast<const float4*>(bp));
+                    if (kk < p.K) v = ld4(bp);
                 } else {
-                    if (kk < p.K) v.x = __ldg(bp);
-                    if (kk + 1 < p.K) v.y = __ldg(bp + 1);
-                    if (kk + 2 < p.K) v.z = __ldg(bp + 2);
-                    if (kk + 3 < p.K) v.w = __ldg(bp + 3);
+                    if (kk < p.K) v.x = ld1(bp);
+                    if (kk + 1 < p.K) v.y = ld1(bp + 1);
+                    if (kk + 2 < p.K) v.z = ld1(bp + 2);
+                    if (kk + 3 < p.K) v.w = ld1(bp + 3);
                 }
             }
             rb[i] = v;
@@ -312,10 +323,10 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
     }
 }
 
-template <int BM, int BN, int BK, int TT, int UNROLL, bool CONV>
+template <int BM, int BN, int BK, int TT, int UNROLL, bool CONV, typename TIn = float>
 cudaError_t simt_launch(const LaunchCtx& c) {
     using Cfg = SimtCfg<BM, BN, BK, TT>;
-    auto kern = simt_gemm_f32_kernel<BM, BN, BK, TT, UNROLL, CONV>;
+    auto kern = simt_gemm_f32_kernel<BM, BN, BK, TT, UNROLL, CONV, TIn>;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -324,8 +335,8 @@ cudaError_t simt_launch(const LaunchCtx& c) {
     }
     const ShapeInfo& s = *c.sh;
     SimtParams p;
-    p.A = (const float*)c.x;
-    p.B = (const float*)c.w;
+    p.A = c.x;
+    p.B = c.w;
     p.C = (float*)c.y;
     p.M = (int)s.M; p.N = (int)s.N; p.K = (int)s.K;
     p.sA = s.M * s.K; p.sB = s.N * s.K; p.sC = s.M * s.N;
@@ -351,6 +362,15 @@ void simt_register() {
     if constexpr (simt_static_ok(BM, BN, BK, TT)) {
         registry_add(kernel_key(CONV ? SK_SIMT_IGEMM_CONV_F32 : SK_SIMT_GEMM_F32, BM, BN, BK, TT, UNROLL),
                      &simt_launch<BM, BN, BK, TT, UNROLL, CONV>);
+    }
+}
+
+// bf16 inputs (CUDA-core FMAs on widened values, fp32 accumulate): implicit-GEMM conv only
+template <int BM, int BN, int BK, int TT, int UNROLL>
+void simt_register_bf16() {
+    if constexpr (simt_static_ok(BM, BN, BK, TT)) {
+        registry_add(kernel_key(SK_SIMT_IGEMM_CONV_BF16, BM, BN, BK, TT, UNROLL),
+                     &simt_launch<BM, BN, BK, TT, UNROLL, true, __nv_bfloat16>);
     }
 }
 

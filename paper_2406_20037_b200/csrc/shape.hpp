@@ -11,7 +11,8 @@ enum SketchId : int32_t {
     SK_SIMT_IGEMM_CONV_F32 = 1,
     SK_TC_GEMM_BF16 = 2,
     SK_TC_IGEMM_CONV_BF16 = 3,
-    SK_COUNT = 4
+    SK_SIMT_IGEMM_CONV_BF16 = 4,
+    SK_COUNT = 5
 };
 
 struct ShapeInfo {  // derived GEMM view of the problem

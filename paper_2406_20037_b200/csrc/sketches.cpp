@@ -38,6 +38,14 @@ static std::vector<SketchDesc> build_catalogue() {
     tcc_vals.push_back({0, 1});
     c.push_back({SK_TC_IGEMM_CONV_BF16, "tc_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tcc_names,
                  tcc_vals});
+    // the SIMT implicit-GEMM sketch on bf16 inputs (widened to fp32 at staging, fp32
+    // accumulate): a second bf16 conv sketch, and the only one for C % 8 != 0 (TMA needs
+    // 16-byte strides); a restricted compile-time lattice
+    const std::vector<std::vector<int32_t>> simt16_vals = {{16, 32, 64, 128}, {16, 32, 64, 128}, {8, 16, 32},
+                                                           {4, 8},            {1, 4},             {1, 4},
+                                                           {1, 2},            {1, 2, 4, 8, 16}};
+    c.push_back({SK_SIMT_IGEMM_CONV_BF16, "simt_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, simt_names,
+                 simt16_vals});
     return c;
 }
 
@@ -91,7 +99,6 @@ bool make_shape_info(int32_t op, const tuner_shape& s, ShapeInfo& o, std::string
 
 static bool simt_valid(const ShapeInfo& sh, const int32_t* v) {
     const int bm = v[0], bn = v[1], bk = v[2], tt = v[3], vec = v[5], split = v[7];
-    if (sh.dtype != TUNER_F32) return false;
     if (tt > bm || tt > bn) return false;
     const int threads = (bm / tt) * (bn / tt);
     if (threads > 1024 || threads < 1) return false;
@@ -139,7 +146,8 @@ bool sketch_valid(int32_t id, const ShapeInfo& sh, const int32_t* v) {
     if (!d || !(d->op_mask & (1 << sh.op)) || d->dtype != sh.dtype) return false;
     switch (id) {
         case SK_SIMT_GEMM_F32:
-        case SK_SIMT_IGEMM_CONV_F32: return simt_valid(sh, v);
+        case SK_SIMT_IGEMM_CONV_F32:
+        case SK_SIMT_IGEMM_CONV_BF16: return simt_valid(sh, v);
         case SK_TC_GEMM_BF16:
         case SK_TC_IGEMM_CONV_BF16: return tc_valid(sh, v);
         default: return false;
