@@ -11,6 +11,8 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <string>
 
 #include "internal.hpp"
 
@@ -55,36 +57,43 @@ tuner_status nccl_fail(ncclResult_t r, const char* what) {
     return fail(TUNER_ENCCL, std::string(what) + ": " + s);
 }
 
-struct NcclComm : Comm {
+// One NCCL communicator per (unique id, rank), created on first use and kept for the
+// life of the process: every tuner of a process group shares it (a communicator per
+// tuner would pay ncclCommInitRank for every layer).
+struct NcclShared {
     ncclComm_t comm = nullptr;
-    cudaStream_t st = nullptr;
+    int world = 1;
     char* d_send = nullptr;
     char* d_recv = nullptr;
     int64_t cap = 0;
-    int world = 1;
-    ~NcclComm() override {
-        if (comm) api().CommDestroy(comm);
-        if (d_send) cudaFree(d_send);
-        if (d_recv) cudaFree(d_recv);
-    }
+};
+
+struct NcclComm : Comm {
+    NcclShared* sh = nullptr;
+    cudaStream_t st = nullptr;
     tuner_status allgather(const void* send, void* recv, int64_t bytes) override {
-        if (bytes > cap) {
-            if (d_send) cudaFree(d_send);
-            if (d_recv) cudaFree(d_recv);
-            if (cudaMalloc(&d_send, bytes) != cudaSuccess || cudaMalloc(&d_recv, bytes * world) != cudaSuccess)
+        if (bytes > sh->cap) {
+            if (sh->d_send) cudaFree(sh->d_send);
+            if (sh->d_recv) cudaFree(sh->d_recv);
+            if (cudaMalloc(&sh->d_send, bytes) != cudaSuccess || cudaMalloc(&sh->d_recv, bytes * sh->world) != cudaSuccess)
                 return fail(TUNER_ENOMEM, "NCCL staging buffers");
-            cap = bytes;
+            sh->cap = bytes;
         }
-        if (cudaMemcpyAsync(d_send, send, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        if (cudaMemcpyAsync(sh->d_send, send, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
             return fail(TUNER_ECUDA, "H2D of result slots");
-        ncclResult_t r = api().AllGather(d_send, d_recv, (size_t)bytes, ncclUint8, comm, st);
+        ncclResult_t r = api().AllGather(sh->d_send, sh->d_recv, (size_t)bytes, ncclUint8, sh->comm, st);
         if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
-        if (cudaMemcpyAsync(recv, d_recv, bytes * world, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        if (cudaMemcpyAsync(recv, sh->d_recv, bytes * sh->world, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
             cudaStreamSynchronize(st) != cudaSuccess)
             return fail(TUNER_ECUDA, "D2H of gathered slots");
         return TUNER_OK;
     }
 };
+
+std::map<std::string, NcclShared*>& comm_cache() {
+    static std::map<std::string, NcclShared*> m;
+    return m;
+}
 }  // namespace
 
 tuner_status nccl_unique_id(void* out128) {
@@ -99,13 +108,28 @@ tuner_status nccl_unique_id(void* out128) {
 
 tuner_status make_nccl_comm(const void* uid, int rank, int world, void* stream, std::unique_ptr<Comm>& out) {
     if (!api().ok) return fail(TUNER_ENCCL, "libnccl.so.2 not found (set DROPLET_NCCL_LIB)");
+    std::string key(static_cast<const char*>(uid), 128);
+    key += std::to_string(rank) + "/" + std::to_string(world);
+    auto& cache = comm_cache();
+    auto it = cache.find(key);
+    NcclShared* sh;
+    if (it != cache.end()) {
+        sh = it->second;
+    } else {
+        sh = new NcclShared();
+        ncclUniqueId id;
+        std::memcpy(&id, uid, 128);
+        ncclResult_t r = api().CommInitRank(&sh->comm, world, id, rank);
+        if (r != ncclSuccess) {
+            delete sh;
+            return nccl_fail(r, "ncclCommInitRank");
+        }
+        sh->world = world;
+        cache[key] = sh;
+    }
     std::unique_ptr<NcclComm> c(new NcclComm());
-    ncclUniqueId id;
-    std::memcpy(&id, uid, 128);
-    ncclResult_t r = api().CommInitRank(&c->comm, world, id, rank);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+    c->sh = sh;
     c->st = (cudaStream_t)stream;
-    c->world = world;
     out = std::move(c);
     return TUNER_OK;
 }

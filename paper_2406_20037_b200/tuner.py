@@ -16,6 +16,8 @@ from . import _lib as L
 
 PointT = Tuple[int, Tuple[int, ...]]
 
+_GROUP_UIDS: Dict[int, object] = {}  # process group -> 128-byte NCCL unique id
+
 
 @dataclass
 class Sample:
@@ -168,12 +170,17 @@ class Tuner:
             return
         backend = dist.get_backend(group)
         if backend == "nccl" and not table_mode:
-            uid = (C.c_char * 128)()
-            if self.rank == 0:
-                L.check(L.lib().tuner_nccl_unique_id(uid))
-            objs = [bytes(uid)]
-            dist.broadcast_object_list(objs, src=dist.get_global_rank(group, 0), group=group)
-            self._uid = (C.c_char * 128).from_buffer_copy(objs[0])
+            # one NCCL unique id per process group: the library keeps one communicator per id,
+            # shared by every tuner of the group (SPMD: every rank creates tuners in the same order)
+            key = id(group)
+            if key not in _GROUP_UIDS:
+                uid = (C.c_char * 128)()
+                if self.rank == 0:
+                    L.check(L.lib().tuner_nccl_unique_id(uid))
+                objs = [bytes(uid)]
+                dist.broadcast_object_list(objs, src=dist.get_global_rank(group, 0), group=group)
+                _GROUP_UIDS[key] = (C.c_char * 128).from_buffer_copy(objs[0])
+            self._uid = _GROUP_UIDS[key]
             o.nccl_unique_id = C.cast(self._uid, C.c_void_p)
             return
 
