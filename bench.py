@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """bench.py — the tuner's hot path on BASELINE.json configs[1]:
 ResNet-18/50 conv2d layers, batch 1, 224x224, fp32: per layer, 300 Ansor-style
-samples + Droplet Search (<= 100 trials) vs a 10,000-trial random baseline run
-by the same harness.
+exploration trials (evolutionary by default) + Droplet Search (<= 100 trials) vs
+a 10,000-trial random baseline run by the same harness (P:329-334, P:397-400,
+P:474).
 
 One *step* = one layer's full tuning job (every §8(a) row): sampler, dispatch,
 execution, verification, timing, sharded all-gather, best-of-N, Droplet, and
