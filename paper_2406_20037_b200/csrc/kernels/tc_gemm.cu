@@ -58,8 +58,9 @@ struct TcParams {
     int m_tiles;                  // 128-row sub-tiles per batch (conv: images x pixel tiles)
     int mp_tiles, n_tiles, batch;  // tiles of the CTA group (CG sub-tiles each)
     int units;                    // SCHED 0: batch * mp_tiles * n_tiles * split
-    int sched;                    // 0 = tiles (+ split-K), 1 = stream-K
-    long long total_iters;        // SCHED 1: tiles * kblocks
+    int sched;                    // 0 = tiles (+ split-K), 1 = stream-K, 2 = full waves by tile + stream-K rest
+    int dp_tiles;                 // SCHED 2: tiles handled whole (a multiple of the group count)
+    long long total_iters;        // SCHED 1/2: streamed k-block iterations (tiles - dp_tiles) * kblocks
     unsigned* flags;              // SCHED 1: per workspace slot (group x CTA): 1 = partial parked
     float* ws;                    // SCHED 1: [slot][128][BN] partial accumulators of tails
     float* C;
@@ -102,10 +103,18 @@ struct SegIter {
             s.nkb = (int)((long long)(kz + 1) * p.kblocks / p.split) - s.kb0;
             s.mode = p.split > 1 ? EPI_RED : EPI_STORE;
             u += G;
+        } else if (u < p.dp_tiles) {  // SCHED 2: the full waves go tile by tile
+            t = u;
+            s.kb0 = 0;
+            s.nkb = p.kblocks;
+            s.mode = EPI_STORE;
+            s.ntails = 0;
+            u += G;
         } else {
             if (cur >= end) return false;
-            t = (int)(cur / p.kblocks);
-            s.kb0 = (int)(cur - (long long)t * p.kblocks);
+            const int tl = (int)(cur / p.kblocks);  // tile index within the streamed remainder
+            t = p.dp_tiles + tl;
+            s.kb0 = (int)(cur - (long long)tl * p.kblocks);
             const long long left = end - cur;
             s.nkb = (int)((long long)(p.kblocks - s.kb0) < left ? (p.kblocks - s.kb0) : left);
             const bool head = s.kb0 == 0, whole = head && s.nkb == p.kblocks;
@@ -113,7 +122,7 @@ struct SegIter {
             // a tail is the FIRST one: heads wait for tails finished early -- no chain
             s.mode = whole ? EPI_STORE : (head ? EPI_HEAD : EPI_TAIL);
             // groups sharing this tile: g(i) = ceil((i+1) G / T) - 1 owns iteration i
-            const long long T = p.total_iters, i0 = (long long)t * p.kblocks, i1 = i0 + p.kblocks - 1;
+            const long long T = p.total_iters, i0 = (long long)tl * p.kblocks, i1 = i0 + p.kblocks - 1;
             s.ntails = (int)(((i1 + 1) * G + T - 1) / T - ((i0 + 1) * G + T - 1) / T);
             cur += s.nkb;
         }
@@ -514,10 +523,15 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     const int tmem_per_sm = (int)(512 / Cfg::TMEM_COLS);
     per_sm = per_sm < tmem_per_sm ? per_sm : tmem_per_sm;
     long long groups = (long long)(c.num_sms / CG) * per_sm;
-    if (c.sched == 1) {
+    if (c.sched >= 1) {
         if (!stream_k_scratch(&p.flags, &p.ws)) return cudaErrorMemoryAllocation;
         if (groups > p.total_iters) groups = p.total_iters;
         if (groups * CG > kStreamKSlots) groups = kStreamKSlots / CG;
+        if (c.sched == 2) {  // whole waves tile by tile, only the remainder streamed (groups with
+                             // an empty share of the remainder simply stop after their waves)
+            p.dp_tiles = (int)((tiles / groups) * groups);
+            p.total_iters = (tiles - p.dp_tiles) * p.kblocks;
+        }
     } else if (groups > units) {
         groups = units;
     }

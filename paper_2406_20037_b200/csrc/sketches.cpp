@@ -25,17 +25,18 @@ static std::vector<SketchDesc> build_catalogue() {
     // BK staged by TMA with 128-byte swizzle, STAGES-deep mbarrier pipeline,
     // split-K (runtime).
     // BM = 256 is the CTA-pair schedule (cta_group::2, UMMA M = 256 over two SMs);
-    // SCHED 0 = persistent tile loop (+ split-K), 1 = stream-K (equal share of all k-blocks).
+    // SCHED 0 = persistent tile loop (+ split-K), 1 = stream-K (equal share of all k-blocks),
+    // 2 = whole waves tile by tile + the remainder tiles stream-K.
     const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED"};
     const std::vector<std::vector<int32_t>> tc_vals = {{128, 256}, {64, 128, 256}, {64, 128}, {2, 3, 4, 6},
-                                                       {1, 2, 4},  {0, 1}};
+                                                       {1, 2, 4},  {0, 1, 2}};
     c.push_back({SK_TC_GEMM_BF16, "tc_gemm_bf16", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL), TUNER_BF16,
                  tc_names, tc_vals});
     // implicit-GEMM conv: the 128-row M tile is a (128/TILE_Q) x TILE_Q rectangle of output pixels
     const std::vector<const char*> tcc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "TILE_Q", "SCHED"};
     std::vector<std::vector<int32_t>> tcc_vals(tc_vals.begin(), tc_vals.end() - 1);
     tcc_vals.push_back({8, 16, 32});
-    tcc_vals.push_back({0, 1});
+    tcc_vals.push_back({0, 1, 2});
     c.push_back({SK_TC_IGEMM_CONV_BF16, "tc_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tcc_names,
                  tcc_vals});
     // the SIMT implicit-GEMM sketch on bf16 inputs (widened to fp32 at staging, fp32
@@ -118,7 +119,7 @@ static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
     const int bm = v[0], bn = v[1], bk = v[2], stages = v[3], split = v[4];
     const int sched = sh.op == TUNER_OP_CONV2D ? v[6] : v[5];
     if (sh.dtype != TUNER_BF16) return false;
-    if (sched == 1 && split != 1) return false;  // stream-K already splits the reduction
+    if (sched >= 1 && split != 1) return false;  // stream-K already splits the reduction
     // TMA needs 16-byte aligned global strides: K (bf16) multiple of 8.
     int64_t ktiles;
     if (sh.op == TUNER_OP_CONV2D) {
