@@ -98,8 +98,9 @@ typedef enum {
     TUNER_S_LAUNCH_FAIL = 4 /* launch error (non-sticky) */
 } tuner_sample_status;
 
-/* One measured candidate (a "sample" in the paper's sense).  cost_ns = median per-launch time (R-M2), +inf
- * unless status == TUNER_S_OK.  rank = the rank that measured it. */
+/* One measured candidate (a "sample" in the paper's sense).  cost_ns =
+ * trimmed-mean per-launch time of the repeats (R-M2), +inf unless status ==
+ * TUNER_S_OK.  rank = the rank that measured it. */
 typedef struct {
     tuner_point pt;
     double cost_ns;
@@ -117,12 +118,15 @@ typedef int (*tuner_allgather_fn)(void* ctx, const void* send, void* recv, int64
 
 typedef struct {
     int32_t warmup;    /* untimed launches before timing (default 2) */
-    int32_t repeats;   /* timed repeats; cost = median over them (default 10) */
+    int32_t repeats;   /* timed repeats; cost = their trimmed mean (default 10) */
     int32_t number;    /* launches per timed repeat, 0 = auto (>= 20 us per repeat) */
     double timeout_ms; /* verify-run time limit (default 1000) */
     uint64_t seed;     /* sampler seed (R-S1) */
     int32_t policy;    /* tuner_ds_policy (default GROW) */
-    double alpha;      /* 0: strict median compare (only value supported) */
+    double alpha;      /* 0: strict cost compare; in (0,1): Droplet moves only when the
+                          neighbour is also significantly faster (two-sided exact
+                          Wilcoxon rank-sum on the repeat timings, p < alpha; P:410,
+                          P:615, R-W1) */
     int32_t max_batch; /* candidates per measured batch / collective (default 512) */
     int32_t verify;    /* 1: verify every candidate (default), 0: skip */
     double early_cut;  /* > 0: a candidate whose verify run is slower than early_cut x
@@ -133,6 +137,10 @@ typedef struct {
      * Copied at create; no device is touched in this mode. */
     const double* cost_table;
     int64_t cost_table_len;
+    /* optional, with cost_table: cost_nsamp (1..16) repeat timings per point,
+     * [point][cost_nsamp] in the table's order, used by the alpha > 0 test */
+    const double* cost_samples;
+    int32_t cost_nsamp;
     /* multi-GPU candidate sharding (R-M1): batch item j is measured by rank
      * j mod world; results are all-gathered.  With world > 1 either
      * `allgather` is set or `nccl_unique_id` (128 bytes from
@@ -214,6 +222,10 @@ tuner_status tuner_measure(tuner_t* t, const tuner_point* pts, int32_t n, tuner_
  * accepted points.  EINVAL if budget < 1; EDIM / ERANGE for a bad start. */
 tuner_status tuner_droplet(tuner_t* t, const tuner_point* start, int32_t budget, tuner_point* traj,
                            int32_t traj_cap, tuner_droplet_report* report);
+
+/* The repeat timings (ns per launch, <= 16) behind a measured point's cost:
+ * out[cap], *n_out = count.  ERANGE if the point was never measured. */
+tuner_status tuner_timings(const tuner_t* t, const tuner_point* pt, float* out, int32_t cap, int32_t* n_out);
 
 /* Best-of-N: first argmin of cost over history (R-B1).  ESTATE if empty. */
 tuner_status tuner_best(const tuner_t* t, tuner_result* out);

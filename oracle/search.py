@@ -27,6 +27,8 @@ from __future__ import annotations
 import math
 from typing import Callable, Dict, List, Optional, Sequence, Tuple
 
+from .stats import wilcoxon_p
+
 Point = Tuple[int, Tuple[int, ...]]
 
 MASK64 = (1 << 64) - 1
@@ -130,13 +132,16 @@ class OracleTuner:
     """
 
     def __init__(self, space: Space, cost: Callable[[Point], float],
-                 valid: Callable[[Point], bool], seed: int = 0):
+                 valid: Callable[[Point], bool], seed: int = 0,
+                 samples: Optional[Callable[[Point], List[float]]] = None):
         self.space = space
         self._cost = cost
         self.valid = valid
         self.rng = SplitMix64(seed)
         self.history: List[Tuple[Point, float]] = []
         self.memo: Dict[Point, float] = {}
+        self._samples = samples                      # per-point repeat timings (statistical mode)
+        self.smemo: Dict[Point, List[float]] = {}
         self.batches: List[List[Point]] = []
         self.generations: List[Tuple[List[Point], List[Point]]] = []  # evolve(): (parents, children)
 
@@ -146,6 +151,8 @@ class OracleTuner:
         for p in batch:
             c = self._cost(p)
             self.memo[p] = c
+            if self._samples is not None:
+                self.smemo[p] = list(self._samples(p))
             self.history.append((p, c))
 
     # Ansor-style proposal (R-S1)
@@ -241,7 +248,7 @@ class OracleTuner:
         return bp, bc
 
     # ------------------------------------------------------------------ Droplet Search
-    def droplet(self, start: Point, budget: int = 100, policy: str = "plain") -> dict:
+    def droplet(self, start: Point, budget: int = 100, policy: str = "plain", alpha: float = 0.0) -> dict:
         """Droplet Search, PAPER.md P:297-304:
 
           1. "At iteration zero, let the best current candidate be" the start.
@@ -275,6 +282,13 @@ class OracleTuner:
         traj = [x]
         rounds = 0
 
+        def better(p: Point, q: Point) -> bool:
+            """p yields a faster kernel than q: strictly lower cost (R-D4) and, with
+            alpha > 0, a significant difference (Wilcoxon rank-sum p < alpha, R-W1)."""
+            if not (self.memo[p] < self.memo[q]):
+                return False
+            return alpha <= 0 or wilcoxon_p(self.smemo[p], self.smemo[q]) < alpha
+
         def new_batch(cands: List[Point]) -> Tuple[List[Point], bool]:
             q = [p for p in cands if p not in self.memo and self.valid(p)]
             room = budget - used
@@ -292,7 +306,7 @@ class OracleTuner:
                 if p in self.memo and self.valid(p):
                     if best_p is None or self.memo[p] < best_c:
                         best_p, best_c = p, self.memo[p]
-            if best_p is None or not (best_c < c):
+            if best_p is None or not better(best_p, x):
                 return self._report(x, c, used, rounds, not trunc, traj)
             prev = x
             x, c = best_p, best_c
@@ -320,7 +334,7 @@ class OracleTuner:
                 used += len(q)
                 rounds += 1
                 for p in ray:
-                    if p in self.memo and self.valid(p) and self.memo[p] < c:
+                    if p in self.memo and self.valid(p) and better(p, x):
                         x, c = p, self.memo[p]
                         traj.append(x)
                     else:

@@ -51,6 +51,7 @@ class Opts(C.Structure):
     _fields_ = [("warmup", C.c_int32), ("repeats", C.c_int32), ("number", C.c_int32), ("timeout_ms", C.c_double),
                 ("seed", C.c_uint64), ("policy", C.c_int32), ("alpha", C.c_double), ("max_batch", C.c_int32),
                 ("verify", C.c_int32), ("early_cut", C.c_double), ("cost_table", C.POINTER(C.c_double)), ("cost_table_len", C.c_int64),
+                ("cost_samples", C.POINTER(C.c_double)), ("cost_nsamp", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("allgather", ALLGATHER_FN), ("allgather_ctx", C.c_void_p), ("x", C.c_void_p), ("w", C.c_void_p),
                 ("y", C.c_void_p), ("y_ref", C.c_void_p), ("y_absref", C.c_void_p), ("stream", C.c_void_p)]
@@ -86,6 +87,7 @@ SIGNATURES = {
     "tuner_droplet": (C.c_int, [C.c_void_p, C.POINTER(Point), C.c_int32, C.POINTER(Point), C.c_int32,
                                 C.POINTER(DropletReport)]),
     "tuner_best": (C.c_int, [C.c_void_p, C.POINTER(Result)]),
+    "tuner_timings": (C.c_int, [C.c_void_p, C.POINTER(Point), C.POINTER(C.c_float), C.c_int32, C.POINTER(C.c_int32)]),
     "tuner_history": (C.c_int, [C.c_void_p, C.POINTER(Result), C.c_int64, C.POINTER(C.c_int64)]),
     "kernel_run": (C.c_int, [C.c_void_p, C.POINTER(Point), C.POINTER(Buffers), C.c_void_p]),
     "tuner_reference": (C.c_int, [C.c_void_p, C.POINTER(Buffers), C.c_void_p, C.c_void_p, C.c_void_p]),

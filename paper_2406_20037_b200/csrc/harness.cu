@@ -282,6 +282,8 @@ struct GpuMeasurer : Measurer {
             }
             if (cut[j]) {
                 out[j].cost_ns = tver[j];
+                out[j].nsamp = 1;
+                out[j].samp[0] = (float)tver[j];
                 continue;
             }
             const size_t b = tb + j * (size_t)(R + 1);
@@ -294,6 +296,8 @@ struct GpuMeasurer : Measurer {
             // R-M2: trimmed mean (drop the fastest and slowest repeat) for R >= 5, median for
             // R < 5 -- the device timer ticks in ~1 us steps, so a plain median of 20 us
             // repeats is quantised to ~5 % and creates artificial ties between neighbours.
+            out[j].nsamp = std::min(Rj, kMaxSamples);
+            for (int r = 0; r < out[j].nsamp; ++r) out[j].samp[r] = (float)per[r];
             std::sort(per.begin(), per.begin() + Rj);
             if (Rj >= 5) {
                 double sum = 0.0;

@@ -59,12 +59,16 @@ struct Pt {
 };
 
 // Per-candidate measurement result.
+static constexpr int kMaxSamples = 16;  // repeat timings kept per candidate (statistical mode)
 struct Result {
     double cost_ns = INFINITY;
     double max_err = 0.0;
     int32_t status = TUNER_S_OK;
     int32_t rank = 0;
+    int32_t nsamp = 0;
+    float samp[kMaxSamples] = {};  // per-launch times of the repeats (ns)
 };
+double wilcoxon_p(const float* a, int n1, const float* b, int n2);
 
 // ---------------------------------------------------------------- sketch catalogue
 bool make_shape_info(int32_t op, const tuner_shape& s, ShapeInfo& out, std::string& why);
@@ -101,7 +105,8 @@ struct Measurer {
 };
 
 struct Tuner;
-std::unique_ptr<Measurer> make_table_measurer(Tuner* t, std::vector<double>&& table);
+std::unique_ptr<Measurer> make_table_measurer(Tuner* t, std::vector<double>&& table, const double* samples,
+                                              int nsamp);
 tuner_status make_gpu_measurer(Tuner* t, std::unique_ptr<Measurer>& out);
 tuner_status gpu_kernel_run(const Tuner* t, const Pt& p, const tuner_buffers* buf, void* stream);
 tuner_status gpu_reference(const Tuner* t, const tuner_buffers* buf, float* y_ref, float* y_absref,
@@ -120,6 +125,7 @@ struct Tuner {
     bool dead = false;
     SplitMix64 rng{0};
     std::vector<tuner_result> history;
+    std::vector<std::vector<float>> hsamples;  // repeat timings per history entry
     std::unordered_map<uint64_t, size_t> memo;  // linear id -> history index
     std::unique_ptr<Measurer> measurer;
     std::unique_ptr<Comm> comm;

@@ -84,15 +84,16 @@ void Tuner::ring(const Pt& x, std::vector<Pt>& out) const {
 
 // ---------------------------------------------------------------- sharded measurement (R-M1)
 namespace {
-struct Slot {  // 32 bytes, keyed by batch index so results are rank-independent
+struct Slot {  // 96 bytes, keyed by batch index so results are rank-independent
     int32_t idx;
     int32_t status;
     double cost_ns;
     double max_err;
     int32_t rank;
-    int32_t pad;
+    int32_t nsamp;
+    float samp[kMaxSamples];
 };
-static_assert(sizeof(Slot) == 32, "slot layout");
+static_assert(sizeof(Slot) == 96, "slot layout");
 }  // namespace
 
 tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
@@ -119,9 +120,17 @@ tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
         const size_t per = (batch.size() + G - 1) / G;
         std::vector<Slot> send(per), recv(per * G);
         for (size_t i = 0; i < per; ++i) {
-            send[i] = Slot{-1, 0, 0.0, 0.0, r, 0};
-            if (i < lres.size())
-                send[i] = Slot{local_idx[i], lres[i].status, lres[i].cost_ns, lres[i].max_err, r, 0};
+            std::memset(&send[i], 0, sizeof(Slot));
+            send[i].idx = -1;
+            send[i].rank = r;
+            if (i < lres.size()) {
+                send[i].idx = local_idx[i];
+                send[i].status = lres[i].status;
+                send[i].cost_ns = lres[i].cost_ns;
+                send[i].max_err = lres[i].max_err;
+                send[i].nsamp = lres[i].nsamp;
+                std::memcpy(send[i].samp, lres[i].samp, sizeof(send[i].samp));
+            }
         }
         if (!comm) return fail(TUNER_ENCCL, "world > 1 but no communicator");
         st = comm->allgather(send.data(), recv.data(), (int64_t)(per * sizeof(Slot)));
@@ -131,7 +140,13 @@ tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
         for (const Slot& s : recv) {
             if (s.idx < 0) continue;
             if ((size_t)s.idx >= batch.size()) return fail(TUNER_ENCCL, "corrupt all-gather slot");
-            res[s.idx] = Result{s.cost_ns, s.max_err, s.status, s.rank};
+            Result& x = res[s.idx];
+            x.cost_ns = s.cost_ns;
+            x.max_err = s.max_err;
+            x.status = s.status;
+            x.rank = s.rank;
+            x.nsamp = s.nsamp < 0 ? 0 : (s.nsamp > kMaxSamples ? kMaxSamples : s.nsamp);
+            std::memcpy(x.samp, s.samp, sizeof(x.samp));
             ++filled;
         }
         if (filled != batch.size()) return fail(TUNER_ENCCL, "all-gather returned an incomplete batch");
@@ -146,6 +161,7 @@ tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
         smp.rank = res[j].rank;
         memo[linear(batch[j])] = history.size();
         history.push_back(smp);
+        hsamples.emplace_back(res[j].samp, res[j].samp + res[j].nsamp);
         if (smp.cost_ns < best_cost) best_cost = smp.cost_ns;
     }
     stats.candidates += (int64_t)batch.size();
@@ -276,6 +292,16 @@ tuner_status Tuner::droplet(const Pt& start, int32_t budget, std::vector<Pt>& tr
         rep.traj_len = (int32_t)traj.size();
         return TUNER_OK;
     };
+    // "yields a faster kernel": strictly lower cost (R-D4) and, with alpha > 0, a
+    // significant difference of the repeat timings (Wilcoxon rank-sum p < alpha, R-W1)
+    auto better = [&](const Pt& p, const Pt& q) {
+        const size_t ip = memo.at(linear(p)), iq = memo.at(linear(q));
+        if (!(history[ip].cost_ns < history[iq].cost_ns)) return false;
+        if (opts.alpha <= 0.0) return true;
+        const auto& a = hsamples[ip];
+        const auto& b = hsamples[iq];
+        return wilcoxon_p(a.data(), (int)a.size(), b.data(), (int)b.size()) < opts.alpha;
+    };
     // the not-yet-measured valid points of `cands`, truncated to the budget left
     auto fresh = [&](const std::vector<Pt>& cands, std::vector<Pt>& q) {
         q.clear();
@@ -301,7 +327,7 @@ tuner_status Tuner::droplet(const Pt& start, int32_t budget, std::vector<Pt>& tr
             double cp = cost(nb[i]);
             if (bi < 0 || cp < bc) { bi = (int)i; bc = cp; }
         }
-        if (bi < 0 || !(bc < c)) return finish(!trunc);
+        if (bi < 0 || !better(nb[bi], x)) return finish(!trunc);
         const Pt prev = x;
         x = nb[bi];
         c = bc;
@@ -329,7 +355,7 @@ tuner_status Tuner::droplet(const Pt& start, int32_t budget, std::vector<Pt>& tr
         used += (int32_t)q.size();
         ++rounds;
         for (const Pt& p : ray) {
-            if (measured(p) && valid(p) && cost(p) < c) {
+            if (measured(p) && valid(p) && better(p, x)) {
                 x = p;
                 c = cost(p);
                 traj.push_back(x);
@@ -346,11 +372,17 @@ namespace {
 struct TableMeasurer : Measurer {
     Tuner* t;
     std::vector<double> table;
+    std::vector<float> samples;  // optional [point][nsamp] repeat timings
+    int nsamp = 0;
     TableMeasurer(Tuner* tt, std::vector<double>&& tab) : t(tt), table(std::move(tab)) {}
     tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out, double) override {
-        out.resize(pts.size());
+        out.assign(pts.size(), Result{});
         for (size_t i = 0; i < pts.size(); ++i) {
-            out[i] = Result{table[t->linear(pts[i])], 0.0, TUNER_S_OK, 0};
+            const uint64_t id = t->linear(pts[i]);
+            out[i].cost_ns = table[id];
+            out[i].status = TUNER_S_OK;
+            out[i].nsamp = nsamp;
+            for (int k = 0; k < nsamp; ++k) out[i].samp[k] = samples[id * nsamp + k];
         }
         return TUNER_OK;
     }
@@ -368,8 +400,14 @@ struct CallbackComm : Comm {
 };
 }  // namespace
 
-std::unique_ptr<Measurer> make_table_measurer(Tuner* t, std::vector<double>&& table) {
-    return std::unique_ptr<Measurer>(new TableMeasurer(t, std::move(table)));
+std::unique_ptr<Measurer> make_table_measurer(Tuner* t, std::vector<double>&& table, const double* samples,
+                                              int nsamp) {
+    std::unique_ptr<TableMeasurer> m(new TableMeasurer(t, std::move(table)));
+    if (samples && nsamp > 0) {
+        m->nsamp = nsamp;
+        m->samples.assign(samples, samples + m->table.size() * (size_t)nsamp);
+    }
+    return std::unique_ptr<Measurer>(m.release());
 }
 
 std::unique_ptr<Comm> make_callback_comm(tuner_allgather_fn fn, void* ctx) {
@@ -422,7 +460,9 @@ extern "C" tuner_status tuner_create(int32_t op, const tuner_shape* shape, const
     if (!(t->opts.early_cut >= 0.0)) return fail(TUNER_EINVAL, "early_cut must be >= 0");
     if (t->opts.repeats < 1 || t->opts.warmup < 0 || t->opts.number < 0 || t->opts.max_batch < 1)
         return fail(TUNER_EINVAL, "repeats >= 1, warmup >= 0, number >= 0, max_batch >= 1 required");
-    if (t->opts.alpha != 0.0) return fail(TUNER_EINVAL, "only alpha = 0 (strict median compare) is supported");
+    if (!(t->opts.alpha >= 0.0 && t->opts.alpha < 1.0)) return fail(TUNER_EINVAL, "alpha must be in [0, 1)");
+    if (t->opts.cost_samples && (t->opts.cost_nsamp < 1 || t->opts.cost_nsamp > kMaxSamples))
+        return fail(TUNER_EINVAL, "cost_nsamp must be in [1, 16]");
     if (t->opts.policy != TUNER_DS_PLAIN && t->opts.policy != TUNER_DS_GROW)
         return fail(TUNER_EINVAL, "unknown Droplet policy");
     if (t->opts.world < 1) t->opts.world = 1;
@@ -493,7 +533,7 @@ extern "C" tuner_status tuner_create(int32_t op, const tuner_shape* shape, const
         std::vector<double> tab(opts->cost_table, opts->cost_table + opts->cost_table_len);
         for (double v : tab)
             if (std::isnan(v)) return fail(TUNER_EINVAL, "NaN in cost table");
-        t->measurer = make_table_measurer(t.get(), std::move(tab));
+        t->measurer = make_table_measurer(t.get(), std::move(tab), opts->cost_samples, opts->cost_nsamp);
     } else {
         if (!opts->x || !opts->w || !opts->y) return fail(TUNER_EINVAL, "measured mode needs x, w, y device buffers");
         tuner_status st = make_gpu_measurer(t.get(), t->measurer);
@@ -596,6 +636,22 @@ extern "C" tuner_status tuner_droplet(tuner_t* t, const tuner_point* start, int3
     if (st != TUNER_OK) return after(t, st);
     if (traj)
         for (int32_t i = 0; i < (int32_t)tr.size() && i < traj_cap; ++i) traj[i] = t->to_public(tr[i]);
+    return TUNER_OK;
+}
+
+extern "C" tuner_status tuner_timings(const tuner_t* tc, const tuner_point* pt, float* out, int32_t cap,
+                                      int32_t* n_out) {
+    Tuner* t = const_cast<tuner_t*>(tc);
+    CHECK_HANDLE(t);
+    if (!pt || !n_out || (cap > 0 && !out)) return fail(TUNER_EINVAL, "NULL argument");
+    tuner_status st;
+    Pt p = t->from_public(*pt, st);
+    if (st != TUNER_OK) return st;
+    auto it = t->memo.find(t->linear(p));
+    if (it == t->memo.end()) return fail(TUNER_ERANGE, "point was never measured");
+    const auto& v = t->hsamples[it->second];
+    *n_out = (int32_t)v.size();
+    for (int32_t i = 0; i < cap && i < (int32_t)v.size(); ++i) out[i] = v[i];
     return TUNER_OK;
 }
 

@@ -116,7 +116,8 @@ class Tuner:
                  seed: int = 0, policy: str = "grow", cost_table=None,
                  x=None, w=None, y=None, y_ref=None, y_absref=None, stream=None, group=None,
                  warmup: int = 2, repeats: int = 10, number: int = 0, max_batch: int = 512,
-                 verify: bool = True, timeout_ms: float = 1000.0, early_cut: float = 0.0):
+                 verify: bool = True, timeout_ms: float = 1000.0, early_cut: float = 0.0,
+                 alpha: float = 0.0, cost_samples=None):
         lib = L.lib()
         self._h = C.c_void_p()
         self.op = op
@@ -138,12 +139,18 @@ class Tuner:
         o.warmup, o.repeats, o.number = warmup, repeats, number
         o.timeout_ms, o.seed, o.policy = timeout_ms, seed, L.POLICY[policy]
         o.max_batch, o.verify, o.early_cut = max_batch, int(bool(verify)), float(early_cut)
+        o.alpha = float(alpha)
         if cost_table is not None:
             import numpy as np
             tab = np.ascontiguousarray(cost_table, dtype=np.float64)
             self._keep.append(tab)
             o.cost_table = tab.ctypes.data_as(C.POINTER(C.c_double))
             o.cost_table_len = tab.size
+            if cost_samples is not None:
+                smp = np.ascontiguousarray(cost_samples, dtype=np.float64)
+                self._keep.append(smp)
+                o.cost_samples = smp.ctypes.data_as(C.POINTER(C.c_double))
+                o.cost_nsamp = smp.shape[1]
         else:
             if x is None or w is None or y is None:
                 raise ValueError("measured mode needs device tensors x, w, y")
@@ -225,6 +232,13 @@ class Tuner:
         return {"best": _unpoint(rep.best), "best_cost": float(rep.best_cost), "trials_used": rep.trials_used,
                 "rounds": rep.rounds, "converged": bool(rep.converged),
                 "traj": [_unpoint(traj[i]) for i in range(min(rep.traj_len, cap))]}
+
+    def timings(self, p: PointT) -> List[float]:
+        """The repeat timings (ns per launch) behind a measured point's cost."""
+        buf = (C.c_float * 16)()
+        n = C.c_int32()
+        L.check(L.lib().tuner_timings(self._h, C.byref(_point(p)), buf, 16, C.byref(n)))
+        return [float(buf[i]) for i in range(n.value)]
 
     def best(self) -> Sample:
         r = L.Result()

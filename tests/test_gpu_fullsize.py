@@ -106,3 +106,21 @@ def test_degenerate_shapes_fp32(op, shape):
     t.run(rep["best"], xd, wd, y)
     torch.cuda.synchronize()
     assert on.max_rel_err(y.cpu().numpy(), yo, ao) <= on.TOL_F32
+
+
+def test_statistical_droplet_measured_mode():
+    # alpha > 0: repeat timings travel with every result; Droplet moves only on
+    # significant improvements (two-sided exact rank-sum, P:410 / P:615)
+    L = RESNET18[1]
+    x, w = layer_tensors(L, 0x5EED)
+    xd, wd = torch.from_numpy(x).to(DEV), torch.from_numpy(w).to(DEV)
+    y = torch.empty(out_shape(L), device=DEV)
+    t = Tuner("conv2d", shape_of(L), x=xd, w=wd, y=y, seed=0, alpha=0.05, early_cut=4.0)
+    t.evolve(100)
+    b = t.best()
+    ts = t.timings(b.point)
+    assert len(ts) == 10 and all(v > 0 for v in ts)
+    rep = t.droplet(b.point, 100)
+    for a, c in zip(rep["traj"], rep["traj"][1:]):
+        from oracle.stats import wilcoxon_p
+        assert wilcoxon_p(t.timings(c), t.timings(a)) < 0.05
