@@ -213,6 +213,16 @@ tuner_status tuner_sample(tuner_t* t, int32_t n, tuner_result* out, int32_t* n_o
 tuner_status tuner_evolve(tuner_t* t, int32_t n, int32_t pop, int32_t elite, tuner_result* out,
                           int32_t* n_out);
 
+/* Multi-layer trial budget (Ansor's task scheduler; reading
+ * R-F3): every layer first explores min(floor(budget/L), 64) trials (at least 1),
+ * then the remaining trials go in `increment`-sized grants to the layer with the
+ * largest weight x best cost, after dropping layers whose weight x best cost is
+ * below drop_frac of the model total.  Exploration is tuner_evolve(pop, elite).
+ * layers: L tuner handles (one per distinct kernel); weights[L] > 0 (occurrences
+ * in the model); trials[L] receives the trials spent per layer.  SPMD-safe. */
+tuner_status tuner_schedule(tuner_t* const* layers, int32_t nlayers, const double* weights, int64_t budget,
+                            int32_t increment, double drop_frac, int32_t pop, int32_t elite, int64_t* trials);
+
 /* Measure an explicit list of points (e.g. exhaustive grid).
  * Already-measured points are returned from the memo and not re-measured. */
 tuner_status tuner_measure(tuner_t* t, const tuner_point* pts, int32_t n, tuner_result* out);

@@ -182,7 +182,8 @@ class OracleTuner:
         """Ansor-style evolution of the annotated population (R-E1), without
         the learned cost model: every child is measured.
 
-        Generation 0 is ``draw(min(pop, n))`` (the sampler, R-S1).  Each later generation
+        Generation 0 is ``draw(min(pop, n))`` (the sampler, R-S1) -- only on a tuner with no
+        finite measurement yet; otherwise the call continues from its elite.  Each later generation
         takes the ``elite`` best measured points of the whole history (cost, then
         measurement order; finite costs only) as parents and produces up to
         min(pop, n - used) new children, each:
@@ -195,9 +196,11 @@ class OracleTuner:
         attempts per generation; an empty generation ends the run.
         """
         out: List[Point] = []
-        first = self.draw(min(pop, n))
-        for i in range(0, len(first), max_batch):
-            self.measure(first[i:i + max_batch])
+        first: List[Point] = []
+        if not any(math.isfinite(c) for _, c in self.history):  # a fresh tuner: generation 0
+            first = self.draw(min(pop, n))                          # (else: continue from the elite)
+            for i in range(0, len(first), max_batch):
+                self.measure(first[i:i + max_batch])
         out += first
         used = len(first)
         while used < n:

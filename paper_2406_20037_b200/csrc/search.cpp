@@ -213,9 +213,13 @@ tuner_status Tuner::measure_chunked(const std::vector<Pt>& pts) {
 tuner_status Tuner::evolve(int32_t n, int32_t pop, int32_t elite, std::vector<Pt>& out) {
     out.clear();
     std::vector<Pt> gen;
-    draw(std::min(pop, n), gen);
-    tuner_status st = measure_chunked(gen);
-    if (st != TUNER_OK) return st;
+    bool any_finite = false;
+    for (const auto& h : history) any_finite |= std::isfinite(h.cost_ns);
+    tuner_status st = TUNER_OK;
+    if (!any_finite) {  // a fresh tuner: generation 0 (else continue from the elite)
+        draw(std::min(pop, n), gen);
+        if ((st = measure_chunked(gen)) != TUNER_OK) return st;
+    }
     out = gen;
     int32_t used = (int32_t)gen.size();
     while (used < n) {
@@ -583,6 +587,71 @@ extern "C" tuner_status tuner_evolve(tuner_t* t, int32_t n, int32_t pop, int32_t
     if (st != TUNER_OK) return after(t, st);
     for (size_t i = 0; i < pts.size(); ++i) fill_sample(t, pts[i], &out[i]);
     *n_out = (int32_t)pts.size();
+    return TUNER_OK;
+}
+
+// ---------------------------------------------------------------- multi-layer budget (R-F3)
+// P:244-248 / P:393-396: initial quota min(K/L, 64) per layer, then the remaining
+// trials in increments to the layer with the largest weight x best cost, after
+// dropping layers below drop_frac of the model total.  Exploration = evolve.
+static double weighted_best(tuner_t* t, double w) {
+    double b = INFINITY;
+    for (const auto& h : t->history)
+        if (h.cost_ns < b) b = h.cost_ns;
+    return w * b;
+}
+
+extern "C" tuner_status tuner_schedule(tuner_t* const* layers, int32_t nlayers, const double* weights, int64_t budget,
+                                       int32_t increment, double drop_frac, int32_t pop, int32_t elite,
+                                       int64_t* trials) {
+    if (!layers || nlayers < 1 || !weights || !trials || budget < 0 || increment < 1 || pop < 1 || elite < 1 ||
+        !(drop_frac >= 0.0))
+        return fail(TUNER_EINVAL, "bad arguments");
+    for (int32_t i = 0; i < nlayers; ++i) {
+        CHECK_HANDLE(layers[i]);
+        if (!(weights[i] > 0.0)) return fail(TUNER_EINVAL, "weights must be > 0");
+        trials[i] = 0;
+    }
+    const int64_t q = std::max<int64_t>(1, std::min<int64_t>(budget / nlayers, 64));
+    int64_t total = 0;
+    std::vector<Pt> got;
+    for (int32_t i = 0; i < nlayers; ++i) {
+        const int64_t n = std::min(q, budget - total);
+        if (n <= 0) break;
+        tuner_status st = layers[i]->evolve((int32_t)n, pop, elite, got);
+        if (st != TUNER_OK) return after(layers[i], st);
+        trials[i] += (int64_t)got.size();
+        total += (int64_t)got.size();
+    }
+    std::vector<int32_t> work;
+    for (int32_t i = 0; i < nlayers; ++i) work.push_back(i);
+    while (total < budget && !work.empty()) {
+        double model = 0.0;
+        for (int32_t i = 0; i < nlayers; ++i) {
+            const double wb = weighted_best(layers[i], weights[i]);
+            if (std::isfinite(wb)) model += wb;
+        }
+        std::vector<int32_t> keep;
+        for (int32_t i : work) {
+            const double wb = weighted_best(layers[i], weights[i]);
+            if (!(std::isfinite(wb) && wb < drop_frac * model)) keep.push_back(i);
+        }
+        work.swap(keep);
+        if (work.empty()) break;
+        int32_t pick = work[0];
+        for (size_t k = 1; k < work.size(); ++k)
+            if (weighted_best(layers[work[k]], weights[work[k]]) > weighted_best(layers[pick], weights[pick]))
+                pick = work[k];
+        const int64_t n = std::min<int64_t>(increment, budget - total);
+        tuner_status st = layers[pick]->evolve((int32_t)n, pop, elite, got);
+        if (st != TUNER_OK) return after(layers[pick], st);
+        if (got.empty()) {
+            work.erase(std::find(work.begin(), work.end(), pick));
+            continue;
+        }
+        trials[pick] += (int64_t)got.size();
+        total += (int64_t)got.size();
+    }
     return TUNER_OK;
 }
 

@@ -84,6 +84,17 @@ def knob_names(sketch: int) -> List[str]:
         i += 1
 
 
+def schedule(tuners: Sequence["Tuner"], weights: Sequence[float], budget: int, increment: int = 16,
+             drop_frac: float = 0.01, pop: int = 64, elite: int = 16) -> List[int]:
+    """Multi-layer trial budget across a model's layers (tuner_schedule); returns trials per layer."""
+    n = len(tuners)
+    hs = (C.c_void_p * n)(*[t._h.value for t in tuners])
+    ws = (C.c_double * n)(*[float(w) for w in weights])
+    out = (C.c_int64 * n)()
+    L.check(L.lib().tuner_schedule(hs, n, ws, int(budget), increment, float(drop_frac), pop, elite, out))
+    return [int(out[i]) for i in range(n)]
+
+
 def global_launch_count() -> int:
     return int(L.lib().tuner_global_launch_count())
 
