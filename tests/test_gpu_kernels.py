@@ -231,3 +231,40 @@ def test_tc_harness_bert_like():
     assert smp and all(s.status == "ok" and s.max_err <= 2e-2 for s in smp), smp[:3]
     rep = t.droplet(t.best().point, 50)
     print("tc best", t.values(rep["best"]), rep["best_cost"], "ns", 2 * m * n * k / rep["best_cost"] / 1e3, "TF")
+
+
+@pytest.mark.parametrize("shape,vals", [
+    ((1, 75, 53, 36), [16, 16, 4, 2, 1, 1, 1, 8]),      # 9 k-tiles, 8 splits of 2: 5 take part
+    ((3, 33, 17, 130), [32, 16, 32, 2, 2, 1, 2, 4]),    # 5 k-tiles, 4 splits of 2: 3 take part
+    ((1, 128, 128, 64), [64, 64, 16, 4, 4, 4, 2, 4]),
+])
+def test_simt_split_k_repeat_and_graph(shape, vals):
+    """Split-K (zeroing + atomic partial sums): back-to-back launches on the same y,
+    launches inside a captured CUDA graph, ragged k splits (CTAs with an empty k
+    range) -- every launch and every replay equals the oracle."""
+    b, m, n, k = shape
+    op = "dense" if b == 1 else "batch_matmul"
+    x, w, yo, ao = gemm_case(b, m, n, k, "uniform", 7 + k)
+    xd, wd = to_dev(x, w)
+    y = torch.full((b, m, n), float("nan"), device=dev())
+    sp = sketch_space(0)
+    t = Tuner(op, {"b": b, "m": m, "n": n, "k": k}, spaces=[(0, sp)], x=xd, w=wd, y=y)
+    p = (0, tuple(sp[d].index(v) for d, v in enumerate(vals)))
+    assert t.valid(p)
+    for _ in range(5):
+        t.run(p, xd, wd, y)  # no zeroing between launches
+        torch.cuda.synchronize()
+        assert on.max_rel_err(y.cpu().numpy().reshape(yo.shape), yo, ao) <= on.TOL_F32
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(3):
+                t.run(p, xd, wd, y, stream=s)
+    for _ in range(4):
+        y.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert on.max_rel_err(y.cpu().numpy().reshape(yo.shape), yo, ao) <= on.TOL_F32
+    r = t.measure([p])[0]
+    assert r.status == "ok" and r.max_err <= on.TOL_F32
