@@ -17,8 +17,8 @@
 // Early cut (opts.early_cut = f > 0, SURVEY d.5): a candidate with t_verify >
 // f x the best cost known is ranked by t_verify alone; one > 1.5x gets 3
 // repeats instead of R.  Candidates that can still win get the full R.
-// Graph capture and instantiation of candidate j+1 on the host overlap the
-// GPU executing candidate j.
+// Graph capture (and update of a cached executable, or instantiation) of
+// candidate j+1 on the host overlap the GPU executing candidate j.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -39,7 +39,8 @@ cudaError_t launch_verify(const float* y, const float* r, const float* a, long l
 void set_capturing(bool on);
 
 static constexpr int kMaxGraphNodes = 8;     // launches per captured graph
-static constexpr double kLightFactor = 1.5;  // early-cut mode: > 1.5x the best -> 3 repeats
+static constexpr double kLightFactor = 1.5;
+static constexpr size_t kExecCache = 16;     // cached timing-graph executables per measurer  // early-cut mode: > 1.5x the best -> 3 repeats
 
 static tuner_status cuda_fail(cudaError_t e, const char* what) {
     return fail(TUNER_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -118,10 +119,40 @@ struct GpuMeasurer : Measurer {
     size_t err_cap = 0;
     double tol;
 
+    // Instantiated timing graphs, reused across candidates: a new candidate's captured
+    // graph is applied to a cached executable of the same topology with
+    // cudaGraphExecUpdate (kernel function, grid and arguments may change), which is
+    // far cheaper on the host than cudaGraphInstantiate.  Launches already enqueued
+    // keep the parameters they were launched with.
+    std::vector<std::pair<size_t, cudaGraphExec_t>> exec_cache;
+
+    cudaError_t exec_for(cudaGraph_t g, cudaGraphExec_t& out) {
+        size_t nn = 0;
+        cudaError_t e = cudaGraphGetNodes(g, nullptr, &nn);
+        if (e != cudaSuccess) return e;
+        for (auto& ce : exec_cache) {
+            if (ce.first != nn) continue;
+            cudaGraphExecUpdateResultInfo info;
+            if (cudaGraphExecUpdate(ce.second, g, &info) == cudaSuccess) {
+                out = ce.second;
+                return cudaSuccess;
+            }
+            cudaGetLastError();  // topology/attributes differ: try the next one
+        }
+        e = cudaGraphInstantiate(&out, g, 0);
+        if (e != cudaSuccess) return e;
+        if (exec_cache.size() < kExecCache) exec_cache.emplace_back(nn, out);
+        else transient.push_back(out);  // destroyed after this phase's synchronisation
+        return cudaSuccess;
+    }
+    std::vector<cudaGraphExec_t> transient;
+
     ~GpuMeasurer() override {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(dev);
+        cudaDeviceSynchronize();
+        for (auto& ce : exec_cache) cudaGraphExecDestroy(ce.second);
         if (own_ref) {
             cudaFree(ref);
             cudaFree(absref);
@@ -276,7 +307,7 @@ struct GpuMeasurer : Measurer {
             set_capturing(false);
             if (e != cudaSuccess) return cuda_fail(e, "graph capture");
             if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamEndCapture");
-            e = cudaGraphInstantiate(&execs[j], g, 0);
+            e = exec_for(g, execs[j]);
             cudaGraphDestroy(g);
             if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
             const size_t b = tb + j * (size_t)(R + 1);
@@ -288,8 +319,8 @@ struct GpuMeasurer : Measurer {
             }
         }
         cudaError_t se = cudaStreamSynchronize(st);
-        for (auto ge : execs)
-            if (ge) cudaGraphExecDestroy(ge);
+        for (auto ge : transient) cudaGraphExecDestroy(ge);
+        transient.clear();
         if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize (timing)");
         std::vector<double> per(R);
         for (size_t j = 0; j < n; ++j) {

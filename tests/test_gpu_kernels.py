@@ -268,3 +268,29 @@ def test_simt_split_k_repeat_and_graph(shape, vals):
         assert on.max_rel_err(y.cpu().numpy().reshape(yo.shape), yo, ao) <= on.TOL_F32
     r = t.measure([p])[0]
     assert r.status == "ok" and r.max_err <= on.TOL_F32
+
+
+def test_batched_costs_match_single_measurements():
+    """Timing graphs are reused across candidates (cudaGraphExecUpdate): costs of an
+    interleaved batch of fast and slow schedules equal their one-at-a-time costs,
+    so no enqueued launch ever runs another candidate's kernel."""
+    m, n, k = 256, 256, 512
+    x, w, yo, ao = gemm_case(1, m, n, k, "uniform", 5)
+    xd, wd = to_dev(x, w)
+    y = torch.empty(1, m, n, device=dev())
+    sp = sketch_space(0)
+    pick = lambda vals: (0, tuple(sp[d].index(v) for d, v in enumerate(vals)))  # noqa: E731
+    fast = [pick([64, 64, 16, 4, 4, 4, 2, 2]), pick([32, 64, 16, 4, 4, 4, 2, 4])]
+    slow = [pick([16, 16, 4, 2, 1, 1, 1, 1]), pick([16, 32, 4, 2, 1, 1, 1, 1])]
+    order = [fast[0], slow[0], fast[1], slow[1]]
+    single = {}
+    for p in order:
+        t1 = Tuner("dense", {"m": m, "n": n, "k": k}, spaces=[(0, sp)], x=xd, w=wd, y=y, seed=1)
+        single[p] = t1.measure([p])[0].cost_ns
+        t1.close()
+    t = Tuner("dense", {"m": m, "n": n, "k": k}, spaces=[(0, sp)], x=xd, w=wd, y=y, seed=2)
+    batch = t.measure(order)
+    assert max(single[p] for p in slow) > 3 * min(single[p] for p in fast)
+    for p, r in zip(order, batch):
+        assert r.status == "ok"
+        assert 0.7 < r.cost_ns / single[p] < 1.4, (t.values(p), r.cost_ns, single[p])
