@@ -19,6 +19,10 @@
  *   conv2d: Y[n,p,q,k] = sum_{r<R,s<S,c<C} X[n, p*sh-ph+r*dh, q*sw-pw+s*dw, c]
  *                                          * W[k,r,s,c]      (NHWC / KRSC / NPQK,
  *           out-of-bounds taps contribute 0; P = (H+2ph-dh(R-1)-1)/sh + 1, Q alike)
+ *   grouped conv2d (G groups; depthwise = G = C = K, the MobileNet/MnasNet/ShuffleNet/
+ *           EfficientNet layers of SURVEY §8(f) f4):
+ *           Y[n,p,q,k] = sum_{r<R,s<S,c<C/G} X[n, p*sh-ph+r*dh, q*sw-pw+s*dw, g*(C/G)+c]
+ *                                          * W[k,r,s,c],  g = k / (K/G)   (W is [K][R][S][C/G])
  * Every function also produces A = the same loops over |X|*|W| (the forward
  * error denominator used by the verification metric, DESIGN.md R-V1).
  */
@@ -107,6 +111,51 @@ void oracle_conv2d_at_f64(const double* X, const double* W, const int64_t* idx, 
         int64_t p = (o / (K * Q)) % P;
         int64_t n = o / (K * Q * P);
         conv_one(X, W, Y + i, A ? A + i : 0, H, Wd, C, R, S, sh, sw, ph, pw, dh, dw, n, p, q, k);
+    }
+}
+
+/* one grouped-conv2d output: the plain (r, s, c) loop over the group's C/G channels */
+static void gconv_one(const double* X, const double* W, double* y, double* a,
+                      int64_t H, int64_t Wd, int64_t C, int64_t K, int64_t G, int64_t R, int64_t S,
+                      int64_t sh, int64_t sw, int64_t ph, int64_t pw, int64_t dh, int64_t dw,
+                      int64_t n, int64_t p, int64_t q, int64_t k) {
+    int64_t cg = C / G;          /* input channels per group */
+    int64_t g = k / (K / G);     /* the group output channel k belongs to */
+    double acc = 0.0, aab = 0.0;
+    for (int64_t r = 0; r < R; ++r) {
+        int64_t h = p * sh - ph + r * dh;
+        for (int64_t s = 0; s < S; ++s) {
+            int64_t w = q * sw - pw + s * dw;
+            if (h < 0 || h >= H || w < 0 || w >= Wd) continue; /* zero padding */
+            const double* xp = X + ((n * H + h) * Wd + w) * C + g * cg;
+            const double* wp = W + ((k * R + r) * S + s) * cg;
+            for (int64_t c = 0; c < cg; ++c) {
+                acc += xp[c] * wp[c];
+                aab += fabs(xp[c]) * fabs(wp[c]);
+            }
+        }
+    }
+    *y = acc;
+    if (a) *a = aab;
+}
+
+/* grouped conv2d (G | C, G | K), NHWC input, W [K][R][S][C/G], NPQK output; with
+   idx != NULL only the outputs at the linear NPQK indices idx[0..cnt) */
+void oracle_gconv2d_f64(const double* X, const double* W, const int64_t* idx, int64_t cnt,
+                        double* Y, double* A, int64_t N, int64_t H, int64_t Wd, int64_t C,
+                        int64_t K, int64_t G, int64_t R, int64_t S, int64_t sh, int64_t sw,
+                        int64_t ph, int64_t pw, int64_t dh, int64_t dw) {
+    int64_t P = out_extent(H, ph, dh, R, sh);
+    int64_t Q = out_extent(Wd, pw, dw, S, sw);
+    int64_t total = idx ? cnt : N * P * Q * K;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < total; ++i) {
+        int64_t o = idx ? idx[i] : i;
+        int64_t k = o % K;
+        int64_t q = (o / K) % Q;
+        int64_t p = (o / (K * Q)) % P;
+        int64_t n = o / (K * Q * P);
+        gconv_one(X, W, Y + i, A ? A + i : 0, H, Wd, C, K, G, R, S, sh, sw, ph, pw, dh, dw, n, p, q, k);
     }
 }
 

@@ -4,7 +4,8 @@ Every function converts its inputs to float64 exactly (fp32 and bf16 values are
 exactly representable in fp64) and calls the direct loops of contractions.c,
 which follow PAPER.md Def. 2.1 ("replaces each linear index ... with
 a loop").  Layouts: dense/bmm X[b,m,k], W[b,n,k], Y[b,m,n]; conv2d X NHWC,
-W KRSC, Y NPQK (DESIGN.md R-C1..R-C3).
+W KRSC, Y NPQK (DESIGN.md R-C1..R-C3); grouped conv W [K][R][S][C/G], depthwise
+= groups C = K with W [C][R][S] (DESIGN.md R-C5).
 """
 from __future__ import annotations
 
@@ -38,6 +39,7 @@ def _lib():
         lib.oracle_conv2d_f64.argtypes = [d, d, d, d] + [i64] * 13
         lib.oracle_conv2d_at_f64.argtypes = [d, d, ctypes.POINTER(i64), i64, d, d] + [i64] * 13
         lib.oracle_bmm_at_f64.argtypes = [d, d, ctypes.POINTER(i64), i64, d, d, i64, i64, i64, i64]
+        lib.oracle_gconv2d_f64.argtypes = [d, d, ctypes.POINTER(i64), i64, d, d] + [i64] * 14
         lib.oracle_num_threads.restype = ctypes.c_int
         _LIB = lib
     return _LIB
@@ -122,3 +124,31 @@ def bmm_at(x, w, idx):
     _lib().oracle_bmm_at_f64(_dp(x), _dp(w), idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                              idx.size, _dp(y), _dp(a), b, m, n, k)
     return y, a
+
+
+def conv2d_grouped(x, w, groups, stride=(1, 1), pad=(0, 0), dil=(1, 1), idx=None):
+    """Grouped conv2d: NHWC x [K][R][S][C/G] -> NPQK (every output, or only the linear
+    NPQK indices ``idx``); returns (Y, A)."""
+    x = _f64(x)
+    w = _f64(w)
+    n, h, wd, c = x.shape
+    k, r, s, cg = w.shape
+    assert c % groups == 0 and k % groups == 0 and cg == c // groups
+    p = conv_out_extent(h, pad[0], dil[0], r, stride[0])
+    q = conv_out_extent(wd, pad[1], dil[1], s, stride[1])
+    if idx is None:
+        shape, ip, cnt = (n, p, q, k), None, 0
+    else:
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        shape, ip, cnt = (idx.size,), idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), idx.size
+    y = np.empty(shape, np.float64)
+    a = np.empty(shape, np.float64)
+    _lib().oracle_gconv2d_f64(_dp(x), _dp(w), ip, cnt, _dp(y), _dp(a), n, h, wd, c, k, groups, r, s,
+                              stride[0], stride[1], pad[0], pad[1], dil[0], dil[1])
+    return y, a
+
+
+def depthwise_conv2d(x, w, stride=(1, 1), pad=(0, 0), dil=(1, 1), idx=None):
+    """Depthwise conv2d (groups = C = K): NHWC x W[C][R][S] -> NPQC; returns (Y, A)."""
+    w = np.asarray(w)
+    return conv2d_grouped(x, w[..., None], w.shape[0], stride, pad, dil, idx)

@@ -105,3 +105,55 @@ def test_verification_metric():
     assert on.max_rel_err(r, r, a) == 0.0
     assert on.max_rel_err(r + np.array([0, 0, 1e-3]), r, a) == pytest.approx(1e-3)
     assert on.max_rel_err(np.array([np.nan, 0, 0]), r, a) == float("inf")
+
+
+GCONV_CASES = [
+    # N, H, W, C, K, G, R, S, stride, pad, dil
+    (2, 9, 7, 6, 6, 6, 3, 3, (1, 1), (1, 1), (1, 1)),       # depthwise 3x3
+    (1, 12, 11, 8, 8, 8, 5, 5, (2, 2), (2, 2), (1, 1)),     # depthwise 5x5 s2 (MnasNet/EfficientNet)
+    (1, 10, 9, 4, 4, 4, 3, 3, (1, 2), (2, 1), (2, 2)),      # dilated, anisotropic
+    (2, 7, 8, 6, 4, 2, 3, 2, (1, 1), (1, 0), (1, 1)),       # 2 groups, 3 -> 2 channels each
+    (1, 6, 6, 5, 10, 5, 1, 1, (1, 1), (0, 0), (1, 1)),      # channel multiplier 2
+]
+
+
+@pytest.mark.parametrize("case", GCONV_CASES)
+def test_grouped_conv_vs_torch_f64(case):
+    n, h, wd, c, k, g, r, s, st, pd, dl = case
+    x, w = tensors([(n, h, wd, c), (k, r, s, c // g)], seed=sum(case[:8]))
+    y, a = oc.conv2d_grouped(x, w, g, st, pd, dl)
+    xt = torch.from_numpy(x.astype(np.float64)).permute(0, 3, 1, 2)
+    wt = torch.from_numpy(w.astype(np.float64)).permute(0, 3, 1, 2)
+    ref = torch.nn.functional.conv2d(xt, wt, stride=st, padding=pd, dilation=dl, groups=g).permute(0, 2, 3, 1)
+    np.testing.assert_allclose(y, ref.numpy(), rtol=1e-12, atol=1e-12)
+    refa = torch.nn.functional.conv2d(xt.abs(), wt.abs(), stride=st, padding=pd, dilation=dl, groups=g)
+    np.testing.assert_allclose(a, refa.permute(0, 2, 3, 1).numpy(), rtol=1e-12, atol=1e-12)
+    sel = np.array([0, y.size // 3, y.size - 1, 7 % y.size])
+    ys, as_ = oc.conv2d_grouped(x, w, g, st, pd, dl, idx=sel)
+    np.testing.assert_array_equal(ys, y.reshape(-1)[sel])
+    np.testing.assert_array_equal(as_, a.reshape(-1)[sel])
+
+
+def test_depthwise_all_ones_closed_form():
+    """All-ones depthwise conv: each output = (# in-bounds rows r) x (# in-bounds cols s)."""
+    n, h, wd, c, r, s, st, pd, dl = 1, 7, 6, 3, 3, 5, (2, 1), (1, 2), (1, 2)
+    y, _ = oc.depthwise_conv2d(np.ones((n, h, wd, c)), np.ones((c, r, s)), st, pd, dl)
+    for p in range(y.shape[1]):
+        rows = sum(1 for i in range(r) if 0 <= p * st[0] - pd[0] + i * dl[0] < h)
+        for q in range(y.shape[2]):
+            cols = sum(1 for j in range(s) if 0 <= q * st[1] - pd[1] + j * dl[1] < wd)
+            assert (y[0, p, q] == rows * cols).all()
+
+
+def test_grouped_conv_special_cases():
+    """groups = 1 is the plain conv2d; a depthwise conv is C independent 1-channel convs."""
+    x, w = tensors([(2, 8, 7, 4), (5, 3, 3, 4)], seed=3)
+    np.testing.assert_array_equal(oc.conv2d_grouped(x, w, 1, (1, 2), (1, 1))[0], oc.conv2d(x, w, (1, 2), (1, 1))[0])
+    xd, wd = tensors([(2, 8, 7, 4), (4, 3, 3)], seed=4)
+    yd, _ = oc.depthwise_conv2d(xd, wd, (2, 1), (1, 1))
+    for ch in range(4):
+        y1, _ = oc.conv2d(xd[..., ch:ch + 1], wd[ch][None, :, :, None], (2, 1), (1, 1))
+        np.testing.assert_array_equal(yd[..., ch], y1[..., 0])
+    xi, wi = tensors([(1, 9, 9, 8), (8, 3, 3)], seed=5, dist="int")
+    yi, _ = oc.depthwise_conv2d(xi, wi, (1, 1), (1, 1))
+    assert np.array_equal(yi, np.round(yi))
