@@ -27,6 +27,9 @@
  *  - conv2d       : Y[n,p,q,k] = sum_{r,s,c} X[n, p*sh-ph+r*dh, q*sw-pw+s*dw, c] W[k,r,s,c]
  *                   X NHWC, W KRSC, Y NPQK, zero padding, groups = 1,
  *                   P = (H + 2ph - dh(R-1) - 1)/sh + 1 (Q alike).
+ *  - depthwise_conv2d : Y[n,p,q,c] = sum_{r,s} X[n, p*sh-ph+r*dh, q*sw-pw+s*dw, c] W[c,r,s]
+ *                   groups = C = K (R-C5; the MobileNet / MnasNet / ShuffleNet /
+ *                   EfficientNet layers): X NHWC, W [C][R][S], Y NPQC.
  *  - TUNER_F32 : x, w, y are float32.  TUNER_BF16 : x, w are bfloat16 (inputs
  *    already rounded), y is float32 (fp32 accumulation, R-C4).
  */
@@ -57,11 +60,17 @@ typedef enum {
     TUNER_ENOMEM = 8
 } tuner_status;
 
-typedef enum { TUNER_OP_DENSE = 0, TUNER_OP_BATCH_MATMUL = 1, TUNER_OP_CONV2D = 2 } tuner_op;
+typedef enum {
+    TUNER_OP_DENSE = 0,
+    TUNER_OP_BATCH_MATMUL = 1,
+    TUNER_OP_CONV2D = 2,
+    TUNER_OP_DEPTHWISE_CONV2D = 3
+} tuner_op;
 typedef enum { TUNER_F32 = 0, TUNER_BF16 = 1 } tuner_dtype;
 
 /* Problem shape.  dense uses m, n, k (b ignored, taken as 1); batch_matmul uses
- * b, m, n, k; conv2d uses N, C, H, W, K, R, S and the stride/pad/dilation.  */
+ * b, m, n, k; conv2d uses N, C, H, W, K, R, S and the stride/pad/dilation;
+ * depthwise_conv2d the same with K == C (else TUNER_EINVAL).  */
 typedef struct {
     int32_t dtype; /* tuner_dtype */
     int64_t b, m, n, k;

@@ -10,3 +10,6 @@ SK_SIMT_GEMM_F32 = 0
 SK_SIMT_IGEMM_CONV_F32 = 1
 SK_TC_GEMM_BF16 = 2
 SK_TC_IGEMM_CONV_BF16 = 3
+SK_SIMT_IGEMM_CONV_BF16 = 4
+SK_SIMT_DWCONV_F32 = 5
+SK_SIMT_DWCONV_BF16 = 6

@@ -16,7 +16,7 @@ MAX_VALUES = 64
 
 OK, EINVAL, EDIM, ERANGE, EOVERFLOW, ESTATE, ECUDA, ENCCL, ENOMEM = range(9)
 STATUS_NAMES = ["OK", "EINVAL", "EDIM", "ERANGE", "EOVERFLOW", "ESTATE", "ECUDA", "ENCCL", "ENOMEM"]
-OP = {"dense": 0, "batch_matmul": 1, "conv2d": 2}
+OP = {"dense": 0, "batch_matmul": 1, "conv2d": 2, "depthwise_conv2d": 3}
 DTYPE = {"f32": 0, "bf16": 1}
 S_OK, S_INVALID, S_TIMEOUT, S_WRONG, S_LAUNCH_FAIL = range(5)
 SAMPLE_STATUS = ["ok", "invalid", "timeout", "wrong", "launch_fail"]

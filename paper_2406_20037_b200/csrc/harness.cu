@@ -54,6 +54,7 @@ static tuner_status cuda_fail(cudaError_t e, const char* what) {
 // launcher + runtime knobs of a point
 struct RuntimeKnobs {
     int split = 1, vec = 1, stages = 1, sched = 0;
+    int dims[3] = {1, 1, 1};
 };
 static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
     int32_t v[TUNER_MAX_KNOBS];
@@ -76,6 +77,12 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
             rk.split = v[4];
             rk.sched = v[6];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[5]));
+        case SK_SIMT_DWCONV_F32:
+        case SK_SIMT_DWCONV_BF16:  // VEC, CT, TQ, QT, PT, SMEM
+            rk.dims[0] = v[1];
+            rk.dims[1] = v[3];
+            rk.dims[2] = v[4];
+            return registry_find(kernel_key(sk, v[0], v[2], v[5], 0, 0));
         default: return nullptr;
     }
 }
@@ -217,6 +224,7 @@ struct GpuMeasurer : Measurer {
             ctx.vec = rk[j].vec;
             ctx.stages = rk[j].stages;
             ctx.sched = rk[j].sched;
+            for (int d = 0; d < 3; ++d) ctx.dims[d] = rk[j].dims[d];
         };
 
         // ---- phase 1: verification run (also the first, untimed-for-cost launch)
@@ -377,6 +385,7 @@ tuner_status gpu_kernel_run(const Tuner* t, const Pt& p, const tuner_buffers* bu
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     LaunchCtx ctx{&t->info, buf->x, buf->w, buf->y, rk.split, rk.vec, rk.stages, rk.sched, (cudaStream_t)stream, nsm};
+    for (int d = 0; d < 3; ++d) ctx.dims[d] = rk.dims[d];
     CU(fn(ctx));
     return TUNER_OK;
 }

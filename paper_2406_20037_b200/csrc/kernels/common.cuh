@@ -20,6 +20,7 @@ struct LaunchCtx {
     int sched;             // runtime SCHED knob (tcgen05: 0 tiles, 1 stream-K)
     cudaStream_t stream;
     int num_sms;
+    int dims[3] = {1, 1, 1};  // runtime thread-block shape knobs (depthwise: CT, QT, PT)
 };
 
 typedef cudaError_t (*LaunchFn)(const LaunchCtx&);

@@ -1,0 +1,225 @@
+// dwconv.cu — sketches SIMT_DWCONV_F32 and SIMT_DWCONV_BF16.
+//
+// Depthwise conv2d (groups = C = K, R-C5): Y[n,p,q,c] = sum_{r,s} X[n, p*sh-ph+r*dh,
+// q*sw-pw+s*dw, c] * W[c,r,s].  Each output reads R*S inputs of ONE channel, so the
+// op has no reduction over channels and no tensor-core shape: it is bound by HBM
+// (|X| + |W| + |Y| once) or, at batch 1, by latency.  The schedule therefore works
+// on coalescing and reuse, not on a GEMM view:
+//   - channels are the fastest NHWC dimension: VEC consecutive channels per thread
+//     (one 32/64/128-bit load per tap), CT threads across channels;
+//   - QT x PT threads across output columns / rows, TQ consecutive output columns
+//     per thread (the taps of neighbouring outputs overlap along q);
+//   - SMEM = 1 stages the CTA's input window (output tile + halo) in shared memory
+//     once, converted to fp32; SMEM = 0 reads taps through L1 (__ldg);
+//   - the CTA's filters are transposed to [r*S+s][channel] in shared memory.
+// Knobs: VEC, TQ, SMEM compile-time; CT, QT, PT runtime (the thread-block shape).
+// fp32 FMAs on the CUDA cores; bf16 inputs are widened at load, fp32 accumulate/out.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace db200 {
+
+struct DwParams {
+    const void* __restrict__ x;
+    const void* __restrict__ w;
+    float* __restrict__ y;
+    int N, H, W, C, R, S, P, Q, sh, sw, ph, pw, dh, dw;
+    int tiles_p;  // ceil(P / PT)
+    int ih, iw;   // SMEM input window: rows, columns
+};
+
+template <typename T, int VEC>
+struct Vec;
+template <>
+struct Vec<float, 1> {
+    static __device__ __forceinline__ void load(const float* p, float* o) { o[0] = __ldg(p); }
+};
+template <>
+struct Vec<float, 2> {
+    static __device__ __forceinline__ void load(const float* p, float* o) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+        o[0] = v.x; o[1] = v.y;
+    }
+};
+template <>
+struct Vec<float, 4> {
+    static __device__ __forceinline__ void load(const float* p, float* o) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    }
+};
+__device__ __forceinline__ float bf_lo(unsigned u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf_hi(unsigned u) { return __uint_as_float(u & 0xFFFF0000u); }
+template <>
+struct Vec<__nv_bfloat16, 1> {
+    static __device__ __forceinline__ void load(const __nv_bfloat16* p, float* o) { o[0] = __bfloat162float(__ldg(p)); }
+};
+template <>
+struct Vec<__nv_bfloat16, 2> {
+    static __device__ __forceinline__ void load(const __nv_bfloat16* p, float* o) {
+        const unsigned u = __ldg(reinterpret_cast<const unsigned*>(p));
+        o[0] = bf_lo(u); o[1] = bf_hi(u);
+    }
+};
+template <>
+struct Vec<__nv_bfloat16, 4> {
+    static __device__ __forceinline__ void load(const __nv_bfloat16* p, float* o) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+        o[0] = bf_lo(u.x); o[1] = bf_hi(u.x); o[2] = bf_lo(u.y); o[3] = bf_hi(u.y);
+    }
+};
+template <typename T>
+__device__ __forceinline__ float to_f32(T v);
+template <>
+__device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <int VEC>
+__device__ __forceinline__ void store_vec(float* p, const float* v) {
+    if constexpr (VEC == 4) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    else if constexpr (VEC == 2) *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    else p[0] = v[0];
+}
+
+template <typename TIn, int VEC, int TQ, bool SMEM>
+__global__ void __launch_bounds__(512) dwconv_kernel(const DwParams p) {
+    extern __shared__ __align__(16) float sm[];
+    const int ct = blockDim.x, qt = blockDim.y, pt = blockDim.z;
+    const int ctv = ct * VEC;  // channels per CTA
+    const int tid = threadIdx.x + ct * (threadIdx.y + qt * threadIdx.z);
+    const int nthr = ct * qt * pt;
+    const int c_cta = blockIdx.x * ctv;
+    const int q_cta = blockIdx.y * qt * TQ;
+    const int n = blockIdx.z / p.tiles_p;
+    const int p_cta = (blockIdx.z % p.tiles_p) * pt;
+    const int RS = p.R * p.S;
+    const TIn* __restrict__ X = (const TIn*)p.x;
+    const TIn* __restrict__ Wt = (const TIn*)p.w;
+
+    // filters of this CTA's channels, transposed to [rs][channel] (zero past C)
+    float* ws = sm;
+    for (int i = tid; i < RS * ctv; i += nthr) {
+        const int rs = i / ctv, cl = i - rs * ctv, c = c_cta + cl;
+        ws[i] = c < p.C ? to_f32(Wt[(long long)c * RS + rs]) : 0.f;
+    }
+    float* xs = ws + RS * ctv;  // SMEM: [ih][iw][ctv]
+    const int h0 = p_cta * p.sh - p.ph, w0 = q_cta * p.sw - p.pw;
+    const long long img = (long long)n * p.H * p.W * p.C;
+    if constexpr (SMEM) {
+        const int cvs = ct;  // VEC-wide channel groups per window position
+        const int total = p.ih * p.iw * cvs;
+        for (int i = tid; i < total; i += nthr) {
+            const int cv = i % cvs, pos = i / cvs;
+            const int col = pos % p.iw, row = pos / p.iw;
+            const int h = h0 + row, w = w0 + col, c = c_cta + cv * VEC;
+            float v[VEC];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) v[e] = 0.f;
+            if ((unsigned)h < (unsigned)p.H && (unsigned)w < (unsigned)p.W && c < p.C)
+                Vec<TIn, VEC>::load(X + img + ((long long)h * p.W + w) * p.C + c, v);
+            float* d = xs + (size_t)pos * ctv + cv * VEC;
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) d[e] = v[e];
+        }
+    }
+    __syncthreads();
+
+    const int cl = threadIdx.x * VEC;  // channel offset inside the CTA
+    const int c = c_cta + cl;
+    const int pp = p_cta + threadIdx.z;
+    const int q0 = q_cta + threadIdx.y * TQ;
+    if (c >= p.C || pp >= p.P || q0 >= p.Q) return;
+
+    float acc[TQ][VEC];
+#pragma unroll
+    for (int t = 0; t < TQ; ++t)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[t][e] = 0.f;
+
+    for (int r = 0; r < p.R; ++r) {
+        const int hr = threadIdx.z * p.sh + r * p.dh;  // window row (SMEM) / offset from h0
+        const int h = h0 + hr;
+        if (!SMEM && (unsigned)h >= (unsigned)p.H) continue;
+        for (int s = 0; s < p.S; ++s) {
+            float wv[VEC];
+            const float* wp = ws + (r * p.S + s) * ctv + cl;
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) wv[e] = wp[e];
+#pragma unroll
+            for (int t = 0; t < TQ; ++t) {
+                const int wc = (threadIdx.y * TQ + t) * p.sw + s * p.dw;  // window column
+                float xv[VEC];
+                if constexpr (SMEM) {
+                    const float* xp = xs + ((size_t)hr * p.iw + wc) * ctv + cl;
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) xv[e] = xp[e];
+                } else {
+                    const int w = w0 + wc;
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) xv[e] = 0.f;
+                    if ((unsigned)w < (unsigned)p.W) Vec<TIn, VEC>::load(X + img + ((long long)h * p.W + w) * p.C + c, xv);
+                }
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) acc[t][e] = fmaf(xv[e], wv[e], acc[t][e]);
+            }
+        }
+    }
+    float* yrow = p.y + (((long long)n * p.P + pp) * p.Q) * p.C + c;
+#pragma unroll
+    for (int t = 0; t < TQ; ++t)
+        if (q0 + t < p.Q) store_vec<VEC>(yrow + (long long)(q0 + t) * p.C, acc[t]);
+}
+
+template <typename TIn, int VEC, int TQ, bool SMEM>
+cudaError_t dwconv_launch(const LaunchCtx& c) {
+    auto kern = dwconv_kernel<TIn, VEC, TQ, SMEM>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    const ShapeInfo& s = *c.sh;
+    const int ct = c.dims[0], qt = c.dims[1], pt = c.dims[2];
+    DwParams p;
+    p.x = c.x;
+    p.w = c.w;
+    p.y = (float*)c.y;
+    p.N = (int)s.n; p.H = (int)s.h; p.W = (int)s.w; p.C = (int)s.c; p.R = (int)s.r; p.S = (int)s.s;
+    p.P = (int)s.p; p.Q = (int)s.q;
+    p.sh = s.sh; p.sw = s.sw; p.ph = s.ph; p.pw = s.pw; p.dh = s.dh; p.dw = s.dw;
+    p.tiles_p = (p.P + pt - 1) / pt;
+    p.ih = (pt - 1) * p.sh + (p.R - 1) * p.dh + 1;
+    p.iw = (qt * TQ - 1) * p.sw + (p.S - 1) * p.dw + 1;
+    const size_t smem = dwconv_smem_bytes(p.R * p.S, ct * VEC, SMEM ? p.ih * p.iw : 0);
+    dim3 grid((unsigned)((p.C + ct * VEC - 1) / (ct * VEC)), (unsigned)((p.Q + qt * TQ - 1) / (qt * TQ)),
+              (unsigned)(p.N * p.tiles_p));
+    kern<<<grid, dim3(ct, qt, pt), smem, c.stream>>>(p);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+template <typename TIn, int VEC, int TQ, bool SMEM>
+static void reg(int32_t sketch) {
+    registry_add(kernel_key(sketch, VEC, TQ, SMEM ? 1 : 0, 0, 0), &dwconv_launch<TIn, VEC, TQ, SMEM>);
+}
+
+template <typename TIn, int VEC>
+static void reg_vec(int32_t sketch) {
+    reg<TIn, VEC, 1, false>(sketch); reg<TIn, VEC, 1, true>(sketch);
+    reg<TIn, VEC, 2, false>(sketch); reg<TIn, VEC, 2, true>(sketch);
+    reg<TIn, VEC, 4, false>(sketch); reg<TIn, VEC, 4, true>(sketch);
+}
+
+void register_dwconv() {
+    reg_vec<float, 1>(SK_SIMT_DWCONV_F32);
+    reg_vec<float, 2>(SK_SIMT_DWCONV_F32);
+    reg_vec<float, 4>(SK_SIMT_DWCONV_F32);
+    reg_vec<__nv_bfloat16, 1>(SK_SIMT_DWCONV_BF16);
+    reg_vec<__nv_bfloat16, 2>(SK_SIMT_DWCONV_BF16);
+    reg_vec<__nv_bfloat16, 4>(SK_SIMT_DWCONV_BF16);
+}
+
+}  // namespace db200

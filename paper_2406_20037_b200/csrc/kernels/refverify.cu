@@ -73,6 +73,35 @@ __global__ void naive_ref_conv(const T* __restrict__ X, const T* __restrict__ W,
     Aabs[o] = (float)aab;
 }
 
+// depthwise conv2d (groups = C = K): W is [C][R][S]
+template <typename T>
+__global__ void naive_ref_dwconv(const T* __restrict__ X, const T* __restrict__ W, float* __restrict__ Y,
+                                 float* __restrict__ Aabs, int N, int H, int Wd, int C, int R, int S, int P, int Q,
+                                 int sh, int sw, int ph, int pw, int dh, int dw) {
+    long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    long long total = (long long)N * P * Q * C;
+    if (o >= total) return;
+    int c = (int)(o % C);
+    int q = (int)((o / C) % Q);
+    int p = (int)((o / ((long long)C * Q)) % P);
+    int n = (int)(o / ((long long)C * Q * P));
+    double acc = 0.0, aab = 0.0;
+    for (int r = 0; r < R; ++r) {
+        int h = p * sh - ph + r * dh;
+        if (h < 0 || h >= H) continue;
+        for (int s = 0; s < S; ++s) {
+            int w = q * sw - pw + s * dw;
+            if (w < 0 || w >= Wd) continue;
+            double xv = as_f64(X[(((long long)n * H + h) * Wd + w) * C + c]);
+            double wv = as_f64(W[((long long)c * R + r) * S + s]);
+            acc += xv * wv;
+            aab += fabs(xv) * fabs(wv);
+        }
+    }
+    Y[o] = (float)acc;
+    Aabs[o] = (float)aab;
+}
+
 __device__ __forceinline__ float err_of(float y, float r, float a) {
     float d = fabsf(y - r) / fmaxf(a, 1e-30f);
     return (isfinite(y) && !isnan(d)) ? d : INFINITY;
@@ -113,7 +142,16 @@ cudaError_t launch_reference(const ShapeInfo& s, const void* x, const void* w, f
     const long long total = s.y_elems;
     const int bs = 128;
     const unsigned grid = (unsigned)((total + bs - 1) / bs);
-    if (s.op == TUNER_OP_CONV2D) {
+    if (s.op == TUNER_OP_DEPTHWISE_CONV2D) {
+        if (s.dtype == TUNER_F32)
+            naive_ref_dwconv<float><<<grid, bs, 0, st>>>((const float*)x, (const float*)w, yref, aref, (int)s.n,
+                                                         (int)s.h, (int)s.w, (int)s.c, (int)s.r, (int)s.s, (int)s.p,
+                                                         (int)s.q, s.sh, s.sw, s.ph, s.pw, s.dh, s.dw);
+        else
+            naive_ref_dwconv<__nv_bfloat16><<<grid, bs, 0, st>>>(
+                (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, yref, aref, (int)s.n, (int)s.h, (int)s.w, (int)s.c,
+                (int)s.r, (int)s.s, (int)s.p, (int)s.q, s.sh, s.sw, s.ph, s.pw, s.dh, s.dw);
+    } else if (s.op == TUNER_OP_CONV2D) {
         if (s.dtype == TUNER_F32)
             naive_ref_conv<float><<<grid, bs, 0, st>>>((const float*)x, (const float*)w, yref, aref, (int)s.n, (int)s.h,
                                                        (int)s.w, (int)s.c, (int)s.k, (int)s.r, (int)s.s, (int)s.p,

@@ -12,6 +12,7 @@ DECL_SIMT(0, 16) DECL_SIMT(0, 32) DECL_SIMT(0, 64) DECL_SIMT(0, 128)
 DECL_SIMT(1, 16) DECL_SIMT(1, 32) DECL_SIMT(1, 64) DECL_SIMT(1, 128)
 void register_tc_gemm();
 void register_simt_bf16_conv();
+void register_dwconv();
 
 static std::unordered_map<uint64_t, LaunchFn>& table() {
     static std::unordered_map<uint64_t, LaunchFn> t;
@@ -24,6 +25,7 @@ static void init_all() {
     register_simt_c1_bm16(); register_simt_c1_bm32(); register_simt_c1_bm64(); register_simt_c1_bm128();
     register_tc_gemm();
     register_simt_bf16_conv();
+    register_dwconv();
 }
 
 uint64_t kernel_key(int32_t sketch, int a, int b, int c, int d, int e) {

@@ -1,5 +1,6 @@
 // shape.hpp — sketch ids and the GEMM view of a problem (kernel-side header).
 #pragma once
+#include <cstddef>
 #include <cstdint>
 
 #include "../../include/tuner.h"
@@ -12,10 +13,16 @@ enum SketchId : int32_t {
     SK_TC_GEMM_BF16 = 2,
     SK_TC_IGEMM_CONV_BF16 = 3,
     SK_SIMT_IGEMM_CONV_BF16 = 4,
-    SK_COUNT = 5
+    SK_SIMT_DWCONV_F32 = 5,
+    SK_SIMT_DWCONV_BF16 = 6,
+    SK_COUNT = 7
 };
 
-struct ShapeInfo {  // derived GEMM view of the problem
+// depthwise sketch: shared-memory bytes of a CTA (filters [R*S][ctv] + input window
+// [win][ctv], fp32); used by the static validity rule and by the launcher
+inline size_t dwconv_smem_bytes(int rs, int ctv, int win) { return (size_t)4 * ((size_t)rs + win) * ctv; }
+
+struct ShapeInfo {  // derived GEMM view of the problem (depthwise: M = n*p*q, N = c, K = r*s)
     int32_t op, dtype;
     int64_t batch, M, N, K;     // GEMM: Y[batch][M][N] = A[batch][M][K] * B[batch][N][K]^T
     // conv

@@ -47,6 +47,16 @@ static std::vector<SketchDesc> build_catalogue() {
                                                            {1, 2},            {1, 2, 4, 8, 16}};
     c.push_back({SK_SIMT_IGEMM_CONV_BF16, "simt_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, simt_names,
                  simt16_vals});
+    // depthwise conv: VEC channels per thread (vector loads along C), CT
+    // threads across channels, TQ output columns per thread, QT x PT threads across
+    // output columns / rows, SMEM = stage the input window in shared memory
+    const std::vector<const char*> dw_names = {"VEC", "CT", "TQ", "QT", "PT", "SMEM"};
+    const std::vector<std::vector<int32_t>> dw_vals = {{1, 2, 4}, {8, 16, 32, 64}, {1, 2, 4},
+                                                       {1, 2, 4, 8}, {1, 2, 4, 8}, {0, 1}};
+    c.push_back({SK_SIMT_DWCONV_F32, "simt_dwconv_f32", 1 << TUNER_OP_DEPTHWISE_CONV2D, TUNER_F32, dw_names,
+                 dw_vals});
+    c.push_back({SK_SIMT_DWCONV_BF16, "simt_dwconv_bf16", 1 << TUNER_OP_DEPTHWISE_CONV2D, TUNER_BF16, dw_names,
+                 dw_vals});
     return c;
 }
 
@@ -75,7 +85,7 @@ bool make_shape_info(int32_t op, const tuner_shape& s, ShapeInfo& o, std::string
         o.y_elems = o.batch * o.M * o.N;
         return true;
     }
-    if (op != TUNER_OP_CONV2D) { why = "unknown op"; return false; }
+    if (op != TUNER_OP_CONV2D && op != TUNER_OP_DEPTHWISE_CONV2D) { why = "unknown op"; return false; }
     if (s.N < 1 || s.C < 1 || s.H < 1 || s.W < 1 || s.K < 1 || s.R < 1 || s.S < 1) {
         why = "conv N, C, H, W, K, R, S must be >= 1"; return false;
     }
@@ -90,9 +100,15 @@ bool make_shape_info(int32_t op, const tuner_shape& s, ShapeInfo& o, std::string
     o.batch = 1;
     o.M = o.n * o.p * o.q;
     o.N = o.k;
-    o.K = o.r * o.s * o.c;
     o.x_elems = o.n * o.h * o.w * o.c;
-    o.w_elems = o.k * o.r * o.s * o.c;
+    if (op == TUNER_OP_DEPTHWISE_CONV2D) {  // groups = C = K (R-C5): W is [C][R][S]
+        if (s.K != s.C) { why = "depthwise_conv2d needs K == C"; return false; }
+        o.K = o.r * o.s;
+        o.w_elems = o.c * o.r * o.s;
+    } else {
+        o.K = o.r * o.s * o.c;
+        o.w_elems = o.k * o.r * o.s * o.c;
+    }
     o.y_elems = o.M * o.N;
     if (o.M >= (1ll << 31) || o.K >= (1ll << 31) || o.N >= (1ll << 31)) { why = "problem too large"; return false; }
     return true;
@@ -142,6 +158,20 @@ static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
     return true;
 }
 
+static bool dw_valid(const ShapeInfo& sh, const int32_t* v) {
+    const int vec = v[0], ct = v[1], tq = v[2], qt = v[3], pt = v[4], smem = v[5];
+    const int threads = ct * qt * pt;
+    if (threads < 32 || threads > 512) return false;  // __launch_bounds__(512): no spills
+    if (sh.c % vec) return false;  // aligned vector loads along C
+    const int64_t ih = (int64_t)(pt - 1) * sh.sh + (sh.r - 1) * sh.dh + 1;
+    const int64_t iw = (int64_t)(qt * tq - 1) * sh.sw + (sh.s - 1) * sh.dw + 1;
+    const size_t bytes = dwconv_smem_bytes((int)(sh.r * sh.s), ct * vec, smem ? (int)(ih * iw) : 0);
+    if (bytes > 227 * 1024) return false;
+    const int64_t tiles_p = (sh.p + pt - 1) / pt;
+    if (sh.n * tiles_p > 65535 || (sh.q + qt * tq - 1) / (qt * tq) > 65535) return false;
+    return true;
+}
+
 bool sketch_valid(int32_t id, const ShapeInfo& sh, const int32_t* v) {
     const SketchDesc* d = sketch_desc(id);
     if (!d || !(d->op_mask & (1 << sh.op)) || d->dtype != sh.dtype) return false;
@@ -151,6 +181,8 @@ bool sketch_valid(int32_t id, const ShapeInfo& sh, const int32_t* v) {
         case SK_SIMT_IGEMM_CONV_BF16: return simt_valid(sh, v);
         case SK_TC_GEMM_BF16:
         case SK_TC_IGEMM_CONV_BF16: return tc_valid(sh, v);
+        case SK_SIMT_DWCONV_F32:
+        case SK_SIMT_DWCONV_BF16: return dw_valid(sh, v);
         default: return false;
     }
 }

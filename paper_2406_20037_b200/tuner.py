@@ -102,9 +102,10 @@ def global_launch_count() -> int:
 def _shape(op: str, shape: Dict, dtype: str) -> L.Shape:
     s = L.Shape()
     s.dtype = L.DTYPE[dtype]
-    if op == "conv2d":
+    if op in ("conv2d", "depthwise_conv2d"):
         s.N, s.C, s.H, s.W = shape["N"], shape["C"], shape["H"], shape.get("W", shape["H"])
-        s.K, s.R, s.S = shape["K"], shape["R"], shape.get("S", shape["R"])
+        s.K = shape["K"] if op == "conv2d" else shape.get("K", shape["C"])
+        s.R, s.S = shape["R"], shape.get("S", shape["R"])
         st, pd, dl = shape.get("stride", (1, 1)), shape.get("pad", (0, 0)), shape.get("dil", (1, 1))
         s.stride_h, s.stride_w = st
         s.pad_h, s.pad_w = pd

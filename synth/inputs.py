@@ -34,6 +34,9 @@ def layer_tensors(layer: dict, seed: int, dist: str = "uniform"):
     if layer["op"] == "conv2d":
         xs = (layer["N"], layer["H"], layer["W"], layer["C"])
         ws = (layer["K"], layer["R"], layer["S"], layer["C"])
+    elif layer["op"] == "depthwise_conv2d":
+        xs = (layer["N"], layer["H"], layer["W"], layer["C"])
+        ws = (layer["C"], layer["R"], layer["S"])
     else:
         b = layer.get("b", 1)
         xs = (b, layer["m"], layer["k"])

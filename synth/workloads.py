@@ -35,6 +35,9 @@ def layer_flops(layer) -> float:
     if layer["op"] == "conv2d":
         P, Q = out_hw(layer)
         return 2.0 * layer["N"] * layer["K"] * P * Q * layer["C"] * layer["R"] * layer["S"]
+    if layer["op"] == "depthwise_conv2d":
+        P, Q = out_hw(layer)
+        return 2.0 * layer["N"] * layer["C"] * P * Q * layer["R"] * layer["S"]
     return 2.0 * layer.get("b", 1) * layer["m"] * layer["n"] * layer["k"]
 
 
