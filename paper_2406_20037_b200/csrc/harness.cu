@@ -78,11 +78,12 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
             rk.sched = v[6];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[5]));
         case SK_SIMT_DWCONV_F32:
-        case SK_SIMT_DWCONV_BF16:  // VEC, CT, TQ, QT, PT, SMEM
+        case SK_SIMT_DWCONV_BF16:  // VEC, CT, TQ, QT, PT, TP, ALG
             rk.dims[0] = v[1];
             rk.dims[1] = v[3];
             rk.dims[2] = v[4];
-            return registry_find(kernel_key(sk, v[0], v[2], v[5], 0, 0));
+            return registry_find(kernel_key(sk, v[0], v[2], v[6], v[5],
+                                            v[6] == 0 ? (int)(t->info.r * 4 + t->info.sh) : 0));
         default: return nullptr;
     }
 }

@@ -4,15 +4,21 @@
 // q*sw-pw+s*dw, c] * W[c,r,s].  Each output reads R*S inputs of ONE channel, so the
 // op has no reduction over channels and no tensor-core shape: it is bound by HBM
 // (|X| + |W| + |Y| once) or, at batch 1, by latency.  The schedule therefore works
-// on coalescing and reuse, not on a GEMM view:
+// on coalescing, reuse and instruction count, not on a GEMM view:
 //   - channels are the fastest NHWC dimension: VEC consecutive channels per thread
 //     (one 32/64/128-bit load per tap), CT threads across channels;
 //   - QT x PT threads across output columns / rows, TQ consecutive output columns
-//     per thread (the taps of neighbouring outputs overlap along q);
-//   - SMEM = 1 stages the CTA's input window (output tile + halo) in shared memory
-//     once, converted to fp32; SMEM = 0 reads taps through L1 (__ldg);
-//   - the CTA's filters are transposed to [r*S+s][channel] in shared memory.
-// Knobs: VEC, TQ, SMEM compile-time; CT, QT, PT runtime (the thread-block shape).
+//     and TP consecutive output rows per thread;
+//   - ALG 0 (register window): filter taps in registers, the thread walks the input
+//     rows its TP x TQ outputs need and loads each row segment ONCE into registers
+//     (every input vector feeds up to TP x TQ outputs); R = S and the stride are
+//     compile-time (3x3 / 5x5, stride 1 / 2: every depthwise layer of the sweep);
+//     no shared memory, no barrier;
+//   - ALG 1 stages the CTA's input window (output tile + halo) in shared memory
+//     once, converted to fp32; ALG 2 reads every tap through L1 (__ldg); both keep
+//     the CTA's filters transposed to [r*S+s][channel] in shared memory and take
+//     any R, S, stride and dilation (TP = 1).
+// Knobs: VEC, TQ, TP, ALG compile-time; CT, QT, PT runtime (the thread-block shape).
 // fp32 FMAs on the CUDA cores; bf16 inputs are widened at load, fp32 accumulate/out.
 #include <cuda_bf16.h>
 
@@ -172,6 +178,87 @@ __global__ void __launch_bounds__(512) dwconv_kernel(const DwParams p) {
         if (q0 + t < p.Q) store_vec<VEC>(yrow + (long long)(q0 + t) * p.C, acc[t]);
 }
 
+// ALG 0: register window.  Compile-time KS = R = S and SH = sh = sw (dilation 1).
+template <typename TIn, int VEC, int TQ, int TP, int KS, int SH>
+__global__ void __launch_bounds__(512) dwconv_win_kernel(const DwParams p) {
+    constexpr int NR = (TP - 1) * SH + KS;  // input rows behind TP output rows
+    constexpr int NC = (TQ - 1) * SH + KS;  // input columns behind TQ output columns
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+    const int q0 = (blockIdx.y * blockDim.y + threadIdx.y) * TQ;
+    const int n = blockIdx.z / p.tiles_p;
+    const int p0 = ((blockIdx.z % p.tiles_p) * blockDim.z + threadIdx.z) * TP;
+    if (c >= p.C || q0 >= p.Q || p0 >= p.P) return;
+    const TIn* __restrict__ X = (const TIn*)p.x + (long long)n * p.H * p.W * p.C + c;
+    const TIn* __restrict__ Wt = (const TIn*)p.w + (long long)c * KS * KS;
+
+    float wr[KS * KS][VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+#pragma unroll
+        for (int rs = 0; rs < KS * KS; ++rs) wr[rs][e] = to_f32(__ldg(Wt + e * KS * KS + rs));
+    float acc[TP][TQ][VEC];
+#pragma unroll
+    for (int a = 0; a < TP; ++a)
+#pragma unroll
+        for (int b = 0; b < TQ; ++b)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[a][b][e] = 0.f;
+
+    const int h0 = p0 * SH - p.ph, w0 = q0 * SH - p.pw;
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+        const int h = h0 + i;
+        const bool hok = (unsigned)h < (unsigned)p.H;
+        float xr[NC][VEC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+            const int w = w0 + j;
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) xr[j][e] = 0.f;
+            if (hok && (unsigned)w < (unsigned)p.W) Vec<TIn, VEC>::load(X + ((long long)h * p.W + w) * p.C, xr[j]);
+        }
+#pragma unroll
+        for (int a = 0; a < TP; ++a) {
+            const int r = i - a * SH;  // compile-time after unrolling
+            if (r < 0 || r >= KS) continue;
+#pragma unroll
+            for (int b = 0; b < TQ; ++b)
+#pragma unroll
+                for (int s = 0; s < KS; ++s)
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) acc[a][b][e] = fmaf(xr[b * SH + s][e], wr[r * KS + s][e], acc[a][b][e]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < TP; ++a) {
+        if (p0 + a >= p.P) break;
+        float* yrow = p.y + (((long long)n * p.P + p0 + a) * p.Q) * p.C + c;
+#pragma unroll
+        for (int b = 0; b < TQ; ++b)
+            if (q0 + b < p.Q) store_vec<VEC>(yrow + (long long)(q0 + b) * p.C, acc[a][b]);
+    }
+}
+
+template <typename TIn, int VEC, int TQ, int TP, int KS, int SH>
+cudaError_t dwconv_win_launch(const LaunchCtx& c) {
+    const ShapeInfo& s = *c.sh;
+    const int ct = c.dims[0], qt = c.dims[1], pt = c.dims[2];
+    DwParams p;
+    p.x = c.x;
+    p.w = c.w;
+    p.y = (float*)c.y;
+    p.N = (int)s.n; p.H = (int)s.h; p.W = (int)s.w; p.C = (int)s.c; p.R = (int)s.r; p.S = (int)s.s;
+    p.P = (int)s.p; p.Q = (int)s.q;
+    p.sh = s.sh; p.sw = s.sw; p.ph = s.ph; p.pw = s.pw; p.dh = s.dh; p.dw = s.dw;
+    p.tiles_p = (p.P + pt * TP - 1) / (pt * TP);
+    p.ih = p.iw = 0;
+    dim3 grid((unsigned)((p.C + ct * VEC - 1) / (ct * VEC)), (unsigned)((p.Q + qt * TQ - 1) / (qt * TQ)),
+              (unsigned)(p.N * p.tiles_p));
+    dwconv_win_kernel<TIn, VEC, TQ, TP, KS, SH><<<grid, dim3(ct, qt, pt), 0, c.stream>>>(p);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
 template <typename TIn, int VEC, int TQ, bool SMEM>
 cudaError_t dwconv_launch(const LaunchCtx& c) {
     auto kern = dwconv_kernel<TIn, VEC, TQ, SMEM>;
@@ -201,16 +288,36 @@ cudaError_t dwconv_launch(const LaunchCtx& c) {
     return cudaGetLastError();
 }
 
+// registry key: (VEC, TQ, ALG, TP, KS * 4 + SH) for ALG 0; (VEC, TQ, ALG, 1, 0) for ALG 1 / 2
 template <typename TIn, int VEC, int TQ, bool SMEM>
-static void reg(int32_t sketch) {
-    registry_add(kernel_key(sketch, VEC, TQ, SMEM ? 1 : 0, 0, 0), &dwconv_launch<TIn, VEC, TQ, SMEM>);
+static void reg_smem(int32_t sketch) {
+    registry_add(kernel_key(sketch, VEC, TQ, SMEM ? 1 : 2, 1, 0), &dwconv_launch<TIn, VEC, TQ, SMEM>);
 }
-
+template <typename TIn, int VEC, int TQ, int TP, int KS, int SH>
+static void reg_win1(int32_t sketch) {
+    if constexpr (dw_win_fits(VEC, TQ, TP, KS, SH))  // the same register rule as sketches.cpp
+        registry_add(kernel_key(sketch, VEC, TQ, 0, TP, KS * 4 + SH), &dwconv_win_launch<TIn, VEC, TQ, TP, KS, SH>);
+}
+template <typename TIn, int VEC, int TQ, int TP>
+static void reg_win(int32_t sketch) {
+    reg_win1<TIn, VEC, TQ, TP, 3, 1>(sketch);
+    reg_win1<TIn, VEC, TQ, TP, 3, 2>(sketch);
+    reg_win1<TIn, VEC, TQ, TP, 5, 1>(sketch);
+    reg_win1<TIn, VEC, TQ, TP, 5, 2>(sketch);
+}
+template <typename TIn, int VEC, int TQ>
+static void reg_tq(int32_t sketch) {
+    reg_smem<TIn, VEC, TQ, true>(sketch);
+    reg_smem<TIn, VEC, TQ, false>(sketch);
+    reg_win<TIn, VEC, TQ, 1>(sketch);
+    reg_win<TIn, VEC, TQ, 2>(sketch);
+    reg_win<TIn, VEC, TQ, 4>(sketch);
+}
 template <typename TIn, int VEC>
 static void reg_vec(int32_t sketch) {
-    reg<TIn, VEC, 1, false>(sketch); reg<TIn, VEC, 1, true>(sketch);
-    reg<TIn, VEC, 2, false>(sketch); reg<TIn, VEC, 2, true>(sketch);
-    reg<TIn, VEC, 4, false>(sketch); reg<TIn, VEC, 4, true>(sketch);
+    reg_tq<TIn, VEC, 1>(sketch);
+    reg_tq<TIn, VEC, 2>(sketch);
+    reg_tq<TIn, VEC, 4>(sketch);
 }
 
 void register_dwconv() {

@@ -22,6 +22,12 @@ enum SketchId : int32_t {
 // [win][ctv], fp32); used by the static validity rule and by the launcher
 inline size_t dwconv_smem_bytes(int rs, int ctv, int win) { return (size_t)4 * ((size_t)rs + win) * ctv; }
 
+// depthwise register-window schedule (ALG 0): taps + one input row segment +
+// accumulators must fit the register budget (fp32 values per thread)
+constexpr bool dw_win_fits(int vec, int tq, int tp, int ks, int sh) {
+    return (ks * ks + (tq - 1) * sh + ks + tp * tq) * vec <= 96;
+}
+
 struct ShapeInfo {  // derived GEMM view of the problem (depthwise: M = n*p*q, N = c, K = r*s)
     int32_t op, dtype;
     int64_t batch, M, N, K;     // GEMM: Y[batch][M][N] = A[batch][M][K] * B[batch][N][K]^T

@@ -49,10 +49,11 @@ static std::vector<SketchDesc> build_catalogue() {
                  simt16_vals});
     // depthwise conv: VEC channels per thread (vector loads along C), CT
     // threads across channels, TQ output columns per thread, QT x PT threads across
-    // output columns / rows, SMEM = stage the input window in shared memory
-    const std::vector<const char*> dw_names = {"VEC", "CT", "TQ", "QT", "PT", "SMEM"};
-    const std::vector<std::vector<int32_t>> dw_vals = {{1, 2, 4}, {8, 16, 32, 64}, {1, 2, 4},
-                                                       {1, 2, 4, 8}, {1, 2, 4, 8}, {0, 1}};
+    // output columns / rows, TP output rows per thread, ALG = 0 register window,
+    // 1 shared-memory window, 2 L1 taps (ALG 1 / 2: TP = 1)
+    const std::vector<const char*> dw_names = {"VEC", "CT", "TQ", "QT", "PT", "TP", "ALG"};
+    const std::vector<std::vector<int32_t>> dw_vals = {{1, 2, 4}, {8, 16, 32, 64}, {1, 2, 4}, {1, 2, 4, 8},
+                                                       {1, 2, 4, 8}, {1, 2, 4}, {0, 1, 2}};
     c.push_back({SK_SIMT_DWCONV_F32, "simt_dwconv_f32", 1 << TUNER_OP_DEPTHWISE_CONV2D, TUNER_F32, dw_names,
                  dw_vals});
     c.push_back({SK_SIMT_DWCONV_BF16, "simt_dwconv_bf16", 1 << TUNER_OP_DEPTHWISE_CONV2D, TUNER_BF16, dw_names,
@@ -159,15 +160,22 @@ static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
 }
 
 static bool dw_valid(const ShapeInfo& sh, const int32_t* v) {
-    const int vec = v[0], ct = v[1], tq = v[2], qt = v[3], pt = v[4], smem = v[5];
+    const int vec = v[0], ct = v[1], tq = v[2], qt = v[3], pt = v[4], tp = v[5], alg = v[6];
     const int threads = ct * qt * pt;
     if (threads < 32 || threads > 512) return false;  // __launch_bounds__(512): no spills
-    if (sh.c % vec) return false;  // aligned vector loads along C
-    const int64_t ih = (int64_t)(pt - 1) * sh.sh + (sh.r - 1) * sh.dh + 1;
-    const int64_t iw = (int64_t)(qt * tq - 1) * sh.sw + (sh.s - 1) * sh.dw + 1;
-    const size_t bytes = dwconv_smem_bytes((int)(sh.r * sh.s), ct * vec, smem ? (int)(ih * iw) : 0);
-    if (bytes > 227 * 1024) return false;
-    const int64_t tiles_p = (sh.p + pt - 1) / pt;
+    if (sh.c % vec) return false;                     // aligned vector loads along C
+    if (alg == 0) {  // register window: compiled for 3x3 / 5x5, stride 1 / 2, no dilation
+        if (sh.r != sh.s || (sh.r != 3 && sh.r != 5) || sh.sh != sh.sw || sh.sh > 2 || sh.dh != 1 || sh.dw != 1)
+            return false;
+        if (!dw_win_fits(vec, tq, tp, (int)sh.r, sh.sh)) return false;  // taps + row segment + accumulators
+    } else {
+        if (tp != 1) return false;
+        const int64_t ih = (int64_t)(pt - 1) * sh.sh + (sh.r - 1) * sh.dh + 1;
+        const int64_t iw = (int64_t)(qt * tq - 1) * sh.sw + (sh.s - 1) * sh.dw + 1;
+        const size_t bytes = dwconv_smem_bytes((int)(sh.r * sh.s), ct * vec, alg == 1 ? (int)(ih * iw) : 0);
+        if (bytes > 227 * 1024) return false;
+    }
+    const int64_t tiles_p = (sh.p + pt * tp - 1) / (pt * tp);
     if (sh.n * tiles_p > 65535 || (sh.q + qt * tq - 1) / (qt * tq) > 65535) return false;
     return true;
 }

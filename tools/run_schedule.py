@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--measure", action="store_true")
+    ap.add_argument("--model", default=None, help="take --layer from this model's sweep table (synth/models.py)")
+    ap.add_argument("--batch", type=int, default=1)
     a = ap.parse_args()
     import torch
 
@@ -27,13 +29,16 @@ def main():
     from synth.workloads import out_hw
 
     allL = {L["name"]: L for L in RESNET18 + RESNET50 + VGG16 + ALEXNET + BERT + [CONFIG1]}
+    if a.model:
+        from synth import model_layers
+        allL = {L["name"]: L for L in model_layers(a.model, a.batch)}
     L = allL[a.layer]
     dev = torch.device("cuda:0")
     x, w = layer_tensors(L, 1)
     xd, wd = torch.from_numpy(x).to(dev), torch.from_numpy(w).to(dev)
     if a.dtype == "bf16":
         xd, wd = xd.to(torch.bfloat16), wd.to(torch.bfloat16)
-    if L["op"] == "conv2d":
+    if L["op"] in ("conv2d", "depthwise_conv2d"):
         P, Q = out_hw(L)
         y = torch.empty((L["N"], P, Q, L["K"]), device=dev)
         shape = {k: L[k] for k in ("N", "C", "H", "W", "K", "R", "S", "stride", "pad", "dil")}
