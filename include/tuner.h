@@ -212,6 +212,13 @@ tuner_status tuner_point_valid(const tuner_t* t, const tuner_point* pt, int32_t*
  * *n_out = number actually drawn (< n only if 64*n draws were exhausted). */
 tuner_status tuner_sample(tuner_t* t, int32_t n, tuner_result* out, int32_t* n_out);
 
+/* Grid search, an exploitation alternative of RQ4 (AutoTVM's grid
+ * tuner): measure the next n statically valid, not-yet-measured points in
+ * enumeration order (sketch order, then row-major linear id, last knob fastest),
+ * continuing from where the previous tuner_grid call stopped.  out: caller array
+ * of n; *n_out < n only when the space is exhausted. */
+tuner_status tuner_grid(tuner_t* t, int32_t n, tuner_result* out, int32_t* n_out);
+
 /* Ansor-style evolutionary exploration (reading R-E1; the learned cost
  * model is out of scope, so every child is measured): generation 0 is
  * tuner_sample's draw of min(pop, n) points; each later generation breeds up to

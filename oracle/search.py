@@ -177,6 +177,23 @@ class OracleTuner:
             self.measure(pts[i:i + max_batch])
         return [(p, self.memo[p]) for p in pts]
 
+    # ------------------------------------------------------------------ grid search (RQ4)
+    def grid(self, n: int, max_batch: int = 512) -> List[Tuple[Point, float]]:
+        """AutoTVM's grid search as an exploitation alternative (RQ4): the next n
+        valid, unmeasured points of ``Space.enumerate()`` order, from a cursor kept across calls."""
+        cur = getattr(self, "_grid_cursor", 0)
+        pts: List[Point] = []
+        while len(pts) < n and cur < self.space.total:
+            p = self.space.point(cur)
+            cur += 1
+            if p in self.memo or not self.valid(p):
+                continue
+            pts.append(p)
+        self._grid_cursor = cur
+        for i in range(0, len(pts), max_batch):
+            self.measure(pts[i:i + max_batch])
+        return [(p, self.memo[p]) for p in pts]
+
     # ------------------------------------------------------------------ evolutionary exploration
     def evolve(self, n: int, pop: int = 64, elite: int = 16, max_batch: int = 512) -> List[Tuple[Point, float]]:
         """Ansor-style evolution of the annotated population (R-E1), without

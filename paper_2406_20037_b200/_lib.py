@@ -85,6 +85,7 @@ SIGNATURES = {
     "tuner_measure": (C.c_int, [C.c_void_p, C.POINTER(Point), C.c_int32, C.POINTER(Result)]),
     "tuner_schedule": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(C.c_double), C.c_int64, C.c_int32,
                                  C.c_double, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
+    "tuner_grid": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Result), C.POINTER(C.c_int32)]),
     "tuner_evolve": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(Result), C.POINTER(C.c_int32)]),
     "tuner_droplet": (C.c_int, [C.c_void_p, C.POINTER(Point), C.c_int32, C.POINTER(Point), C.c_int32,
                                 C.POINTER(DropletReport)]),

@@ -131,6 +131,7 @@ struct Tuner {
     std::unique_ptr<Comm> comm;
     tuner_stats stats{};
     double best_cost = INFINITY;
+    uint64_t grid_cursor = 0;  // next union linear id tuner_grid examines
 
     uint64_t linear(const Pt& p) const;
     Pt from_public(const tuner_point& tp, tuner_status& st) const;  // validates dims/ranges
@@ -145,6 +146,7 @@ struct Tuner {
     tuner_status draw(int32_t n, std::vector<Pt>& out);
     tuner_status measure_chunked(const std::vector<Pt>& pts);
     tuner_status evolve(int32_t n, int32_t pop, int32_t elite, std::vector<Pt>& out);
+    void grid(int32_t n, std::vector<Pt>& out);
     tuner_status droplet(const Pt& start, int32_t budget, std::vector<Pt>& traj,
                          tuner_droplet_report& rep);
 };

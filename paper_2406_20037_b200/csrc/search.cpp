@@ -202,6 +202,30 @@ tuner_status Tuner::measure_chunked(const std::vector<Pt>& pts) {
     return TUNER_OK;
 }
 
+// ---------------------------------------------------------------- grid search
+// AutoTVM's grid search as an exploitation alternative (RQ4): the next n
+// statically valid, unmeasured points in enumeration order (union linear id: sketch
+// order, then row-major, last knob fastest), from a cursor kept across calls.
+void Tuner::grid(int32_t n, std::vector<Pt>& out) {
+    out.clear();
+    const uint64_t end = spaces.back().offset + spaces.back().size;
+    while ((int32_t)out.size() < n && grid_cursor < end) {
+        const uint64_t id = grid_cursor++;
+        Pt p;
+        while (p.pos + 1 < (int32_t)spaces.size() && id >= spaces[p.pos + 1].offset) ++p.pos;
+        const SketchSpace& s = spaces[p.pos];
+        p.n = s.nknobs();
+        uint64_t rem = id - s.offset;
+        for (int d = p.n - 1; d >= 0; --d) {
+            const uint64_t card = s.values[d].size();
+            p.idx[d] = (int32_t)(rem % card);
+            rem /= card;
+        }
+        if (memo.count(id) || !valid(p)) continue;
+        out.push_back(p);
+    }
+}
+
 // ---------------------------------------------------------------- evolutionary exploration
 // Ansor's evolution of annotated sketches without the learned cost
 // model (every child is measured), R-E1: generation 0 = the sampler; then each
@@ -572,6 +596,19 @@ extern "C" tuner_status tuner_sample(tuner_t* t, int32_t n, tuner_result* out, i
         tuner_status st = t->measure_batch(b);
         if (st != TUNER_OK) return after(t, st);
     }
+    for (size_t i = 0; i < pts.size(); ++i) fill_sample(t, pts[i], &out[i]);
+    *n_out = (int32_t)pts.size();
+    return TUNER_OK;
+}
+
+extern "C" tuner_status tuner_grid(tuner_t* t, int32_t n, tuner_result* out, int32_t* n_out) {
+    CHECK_HANDLE(t);
+    if (n < 0 || (n > 0 && !out) || !n_out) return fail(TUNER_EINVAL, "bad arguments");
+    *n_out = 0;
+    std::vector<Pt> pts;
+    t->grid(n, pts);
+    tuner_status st = t->measure_chunked(pts);
+    if (st != TUNER_OK) return after(t, st);
     for (size_t i = 0; i < pts.size(); ++i) fill_sample(t, pts[i], &out[i]);
     *n_out = (int32_t)pts.size();
     return TUNER_OK;

@@ -222,6 +222,13 @@ class Tuner:
         L.check(L.lib().tuner_sample(self._h, n, out, C.byref(got)))
         return [_sample(out[i]) for i in range(got.value)]
 
+    def grid(self, n: int) -> List[Sample]:
+        """Grid search: the next n valid unmeasured points in enumeration order (tuner_grid)."""
+        out = (L.Result * max(1, n))()
+        got = C.c_int32()
+        L.check(L.lib().tuner_grid(self._h, n, out, C.byref(got)))
+        return [_sample(out[i]) for i in range(got.value)]
+
     def evolve(self, n: int, pop: int = 64, elite: int = 16) -> List[Sample]:
         """Ansor-style evolutionary exploration (tuner_evolve)."""
         out = (L.Result * max(1, n))()
