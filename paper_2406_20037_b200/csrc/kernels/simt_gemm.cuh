@@ -140,28 +140,58 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
     // staging registers: each slot holds 4 consecutive k of one row
     float4 ra[Cfg::SA], rb[Cfg::SB];
 
+    // implicit GEMM: a thread's A slots keep the same rows for every k-tile, so
+    // with few slots their (image base, h0, w0) live in registers, not smem
+    constexpr bool ROWREG = CONV && Cfg::SA <= 4;
+    constexpr int NRR = ROWREG ? Cfg::SA : 1;
+    int rbase[NRR], rh0[NRR], rw0[NRR];
+    if constexpr (ROWREG) {
+#pragma unroll
+        for (int i = 0; i < Cfg::SA; ++i) {
+            const int e = tid + i * NT, row = e / KV;
+            const bool in = e < BM * KV;
+            rbase[i] = in ? rowinfo[row] : 0;
+            rh0[i] = in ? rowinfo[BM + row] : -(1 << 29);
+            rw0[i] = in ? rowinfo[2 * BM + row] : 0;
+        }
+    }
+    auto row_base = [&](int i, int row) -> int {
+        if constexpr (ROWREG) return rbase[i]; else return rowinfo[row];
+    };
+    auto row_h0 = [&](int i, int row) -> int {
+        if constexpr (ROWREG) return rh0[i]; else return rowinfo[BM + row];
+    };
+    auto row_w0 = [&](int i, int row) -> int {
+        if constexpr (ROWREG) return rw0[i]; else return rowinfo[2 * BM + row];
+    };
+
     // one A element (dense or implicit GEMM), zero outside the problem
-    auto a_elem = [&](int row, int kk, RSC rsc) -> float {
+    auto a_elem = [&](int i, int row, int kk, RSC rsc) -> float {
         if (kk >= p.K) return 0.f;
         if constexpr (CONV) {
-            const int h = rowinfo[BM + row] + rsc.r * p.dh;
-            const int w = rowinfo[2 * BM + row] + rsc.s * p.dw;
+            const int h = row_h0(i, row) + rsc.r * p.dh;
+            const int w = row_w0(i, row) + rsc.s * p.dw;
             if ((unsigned)h >= (unsigned)p.H || (unsigned)w >= (unsigned)p.W) return 0.f;
-            return ld1(A + rowinfo[row] + (h * p.W + w) * p.Cin + rsc.c);
+            return ld1(A + row_base(i, row) + (h * p.W + w) * p.Cin + rsc.c);
         } else {
             return ld1(A + (long long)(m0 + row) * p.K + kk);
         }
     };
 
+    // (r, s, c) of the next k-tile's first reduction index: k-tiles are loaded in
+    // order, so it is carried forward by BK instead of divided out per tile
+    RSC knext{0, 0, 0};
+    if constexpr (CONV) {
+        const int k0 = kt_begin * BK, rs = k0 / p.Cin;
+        knext.c = k0 - rs * p.Cin;
+        knext.s = rs % p.S;
+        knext.r = rs / p.S;
+    }
+
     auto gload = [&](int kt) {
         const int k0 = kt * BK;
-        RSC base{0, 0, 0};
-        if constexpr (CONV) {
-            int rs = k0 / p.Cin;
-            base.c = k0 - rs * p.Cin;
-            base.s = rs % p.S;
-            base.r = rs / p.S;
-        }
+        const RSC base = knext;
+        if constexpr (CONV) knext = rsc_advance(knext, BK, p.Cin, p.S);
 #pragma unroll
         for (int i = 0; i < Cfg::SA; ++i) {
             const int e = tid + i * NT;
@@ -174,22 +204,22 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
                 if (p.vec4) {  // VEC = 4: one 128-bit load (K or C is a multiple of 4)
                     if (kk < p.K) {
                         if constexpr (CONV) {
-                            const int h = rowinfo[BM + row] + rsc.r * p.dh;
-                            const int w = rowinfo[2 * BM + row] + rsc.s * p.dw;
+                            const int h = row_h0(i, row) + rsc.r * p.dh;
+                            const int w = row_w0(i, row) + rsc.s * p.dw;
                             if ((unsigned)h < (unsigned)p.H && (unsigned)w < (unsigned)p.W)
-                                v = ld4(A + rowinfo[row] + (h * p.W + w) * p.Cin + rsc.c);
+                                v = ld4(A + row_base(i, row) + (h * p.W + w) * p.Cin + rsc.c);
                         } else {
                             v = ld4(A + (long long)(m0 + row) * p.K + kk);
                         }
                     }
                 } else {  // VEC = 1: four scalar loads
-                    v.x = a_elem(row, kk, rsc);
+                    v.x = a_elem(i, row, kk, rsc);
                     if constexpr (CONV) rsc = rsc_advance(rsc, 1, p.Cin, p.S);
-                    v.y = a_elem(row, kk + 1, rsc);
+                    v.y = a_elem(i, row, kk + 1, rsc);
                     if constexpr (CONV) rsc = rsc_advance(rsc, 1, p.Cin, p.S);
-                    v.z = a_elem(row, kk + 2, rsc);
+                    v.z = a_elem(i, row, kk + 2, rsc);
                     if constexpr (CONV) rsc = rsc_advance(rsc, 1, p.Cin, p.S);
-                    v.w = a_elem(row, kk + 3, rsc);
+                    v.w = a_elem(i, row, kk + 3, rsc);
                 }
             }
             ra[i] = v;
