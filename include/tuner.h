@@ -153,7 +153,8 @@ typedef struct {
     /* multi-GPU candidate sharding (R-M1): batch item j is measured by rank
      * j mod world; results are all-gathered.  With world > 1 either
      * `allgather` is set or `nccl_unique_id` (128 bytes from
-     * tuner_nccl_unique_id on rank 0) is given and NCCL is used. */
+     * tuner_nccl_unique_id on rank 0) is given and NCCL is used (else
+     * TUNER_EINVAL).  An exchange given at world 1 is used as well. */
     int32_t rank, world;
     const void* nccl_unique_id;
     tuner_allgather_fn allgather;

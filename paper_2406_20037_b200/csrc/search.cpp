@@ -114,7 +114,7 @@ tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
     if (st != TUNER_OK) return st;
     for (auto& x : lres) x.rank = r;
     std::vector<Result> res(batch.size());
-    if (G == 1) {
+    if (!comm) {
         res = lres;
     } else {
         const size_t per = (batch.size() + G - 1) / G;
@@ -132,7 +132,6 @@ tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
                 std::memcpy(send[i].samp, lres[i].samp, sizeof(send[i].samp));
             }
         }
-        if (!comm) return fail(TUNER_ENCCL, "world > 1 but no communicator");
         st = comm->allgather(send.data(), recv.data(), (int64_t)(per * sizeof(Slot)));
         if (st != TUNER_OK) return st;
         stats.collectives++;
@@ -545,15 +544,15 @@ extern "C" tuner_status tuner_create(int32_t op, const tuner_shape* shape, const
     }
     t->total = off;
     t->rng = SplitMix64(opts->seed);
-    if (t->opts.world > 1) {
-        if (opts->allgather) {
-            t->comm = make_callback_comm(opts->allgather, opts->allgather_ctx);
-        } else if (opts->nccl_unique_id) {
-            tuner_status st = make_nccl_comm(opts->nccl_unique_id, t->opts.rank, t->opts.world, opts->stream, t->comm);
-            if (st != TUNER_OK) return st;
-        } else {
-            return fail(TUNER_EINVAL, "world > 1 needs an allgather callback or an NCCL unique id");
-        }
+    // the exchange step (R-M1): a caller-supplied host all-gather, or NCCL from a unique
+    // id; an exchange given at world 1 is used too (one rank gathers its own slots)
+    if (opts->allgather) {
+        t->comm = make_callback_comm(opts->allgather, opts->allgather_ctx);
+    } else if (opts->nccl_unique_id) {
+        tuner_status st = make_nccl_comm(opts->nccl_unique_id, t->opts.rank, t->opts.world, opts->stream, t->comm);
+        if (st != TUNER_OK) return st;
+    } else if (t->opts.world > 1) {
+        return fail(TUNER_EINVAL, "world > 1 needs an allgather callback or an NCCL unique id");
     }
     if (t->table_mode) {
         if ((uint64_t)opts->cost_table_len != t->total)

@@ -185,9 +185,9 @@ class Tuner:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         o.world, o.rank = self.world, self.rank
-        if self.world == 1:
-            return
         backend = dist.get_backend(group)
+        if self.world == 1 and backend != "nccl":
+            return  # nothing to exchange (a 1-rank NCCL group still runs the collective path)
         if backend == "nccl" and not table_mode:
             # one NCCL unique id per process group: the library keeps one communicator per id,
             # shared by every tuner of the group (SPMD: every rank creates tuners in the same order)

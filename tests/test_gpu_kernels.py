@@ -294,3 +294,41 @@ def test_batched_costs_match_single_measurements():
     for p, r in zip(order, batch):
         assert r.status == "ok"
         assert 0.7 < r.cost_ns / single[p] < 1.4, (t.values(p), r.cost_ns, single[p])
+
+
+def test_nccl_exchange_path_world1():
+    """The NCCL all-gather path (dlopen'ed libnccl, communicator from a unique id,
+    96-B result slots) end to end on a 1-rank NCCL group: every batch goes
+    through the collective, and the search behaves as without it."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev())
+    try:
+        m, n, k = 96, 80, 72
+        x, w, yo, ao = gemm_case(1, m, n, k, "uniform", 21)
+        xd, wd = to_dev(x, w)
+        y = torch.empty(1, m, n, device=dev())
+        t = Tuner("dense", {"m": m, "n": n, "k": k}, spaces=[(0, sketch_space(0))], x=xd, w=wd, y=y, seed=4,
+                  group=dist.group.WORLD, max_batch=16)
+        smp = t.sample(40)
+        rep = t.droplet(t.best().point, 20)
+        st = t.stats()
+        assert st["collectives"] >= 3 + rep["rounds"] - 1
+        assert len(smp) == 40 and all(s.status == "ok" and s.rank == 0 for s in smp)
+        assert all(np.isfinite(s.cost_ns) for s in t.history())
+        t.run(rep["best"], xd, wd, y)
+        torch.cuda.synchronize()
+        assert on.max_rel_err(y.cpu().numpy().reshape(yo.shape), yo, ao) <= on.TOL_F32
+        t.close()
+    finally:
+        dist.destroy_process_group()
