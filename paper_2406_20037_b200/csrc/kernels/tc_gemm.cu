@@ -316,7 +316,9 @@ __global__ void __launch_bounds__(192, 1)
                 epi_bar(1);
             }
             const bool red = w.mode == EPI_RED;
-            float* crow = w.mode == EPI_TAIL ? p.ws + ((long long)slot * 128 + trow) * BN  // parked partial
+            // a parked partial is stored thread-major, [BN/16][128 rows][16], so each warp
+            // writes (and its head later reads) 2 KB contiguous per 16-column group
+            float* crow = w.mode == EPI_TAIL ? p.ws + (long long)slot * 128 * 256 + trow * 16
                                              : p.C + orow * p.N;
             const int n0 = w.mode == EPI_TAIL ? 0 : w.nt * BN;
             const bool live = w.mode == EPI_TAIL ? true : row_ok;
@@ -335,7 +337,8 @@ __global__ void __launch_bounds__(192, 1)
                     if (!live || n >= ncols) continue;
                     if (w.mode == EPI_HEAD) {  // add the tails' partials (same rows, same columns)
                         for (int tl = 1; tl <= w.ntails; ++tl) {
-                            const float* pp = p.ws + ((long long)(slot + tl * CG) * 128 + trow) * BN + c0 + g * 16;
+                            const float* pp = p.ws + (long long)(slot + tl * CG) * 128 * 256 +
+                                              (long long)((c0 + g * 16) / 16) * (128 * 16) + trow * 16;
 #pragma unroll
                             for (int v = 0; v < 4; ++v) {
                                 const float4 x = __ldcg(reinterpret_cast<const float4*>(pp) + v);
@@ -347,12 +350,13 @@ __global__ void __launch_bounds__(192, 1)
                         }
                     }
                     if ((vec_ok || w.mode == EPI_TAIL) && n + 16 <= ncols) {
+                        float* dst = w.mode == EPI_TAIL ? crow + (long long)(n / 16) * (128 * 16) : crow + n;
 #pragma unroll
                         for (int v = 0; v < 4; ++v) {
                             float4 f = make_float4(__uint_as_float(r[g][4 * v]), __uint_as_float(r[g][4 * v + 1]),
                                                    __uint_as_float(r[g][4 * v + 2]), __uint_as_float(r[g][4 * v + 3]));
-                            if (red) tc::red_add_v4(crow + n + 4 * v, f.x, f.y, f.z, f.w);
-                            else *reinterpret_cast<float4*>(crow + n + 4 * v) = f;
+                            if (red) tc::red_add_v4(dst + 4 * v, f.x, f.y, f.z, f.w);
+                            else *reinterpret_cast<float4*>(dst + 4 * v) = f;
                         }
                     } else {
 #pragma unroll
@@ -425,7 +429,8 @@ static bool encode(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* 
 // stream-K scratch, per device, allocated once (outside graph capture: the first
 // launch of a schedule is never captured): kStreamKSlots flags, zeroed once and
 // left at 0 by every launch (heads re-arm their tails' flags), and one
-// 128 x 256 fp32 partial-accumulator slot per (group, CTA)
+// 128 x 256 fp32 partial-accumulator slot per (group, CTA), thread-major
+// ([16-column group][row][16]) so parking and fix-up are coalesced
 static bool stream_k_scratch(unsigned** flags, float** ws) {
     static unsigned* fl[64] = {};
     static float* w[64] = {};
