@@ -31,7 +31,11 @@
 // Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
 // warps 2..5 = epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).
 // Knobs: BM, BN, BK, STAGES, SPLIT_K, TILE_Q (conv only).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "tc_common.cuh"
@@ -48,7 +52,12 @@ struct TcCfg {
     static constexpr int B_BYTES = BNC * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
-    static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+    // epilogue staging for TMA stores: per epilogue warp two 32-row x 16-column fp32
+    // boxes (double-buffered against the asynchronous bulk stores)
+    static constexpr int EPI_BOX = 32 * 16;
+    static constexpr int EPI_BYTES = 4 * 2 * EPI_BOX * 4;
+    static_assert(EPI_BYTES == kTcEpiBytes, "epilogue staging size");
+    static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256 + EPI_BYTES;
     static constexpr int THREADS = 192;
 };
 
@@ -60,10 +69,12 @@ struct TcParams {
     int units;                    // SCHED 0: batch * mp_tiles * n_tiles * split
     int sched;                    // 0 = tiles (+ split-K), 1 = stream-K, 2 = full waves by tile + stream-K rest
     int dp_tiles;                 // SCHED 2: tiles handled whole (a multiple of the group count)
+    int rem_tiles, rem_chunks;    // SCHED 2: remainder tiles and k-chunks per remainder tile
     long long total_iters;        // SCHED 1/2: streamed k-block iterations (tiles - dp_tiles) * kblocks
     unsigned* flags;              // SCHED 1: per workspace slot (group x CTA): 1 = partial parked
     float* ws;                    // SCHED 1: [slot][128][BN] partial accumulators of tails
     float* C;
+    unsigned long long* trace;  // debug (DB200_TC_TRACE): [CTA][16] globaltimer stamps, else nullptr
     // implicit GEMM
     int P, Q, S, CB;  // CB = channel blocks of BK per tap
     int sh, sw, ph, pw, dh, dw;
@@ -79,7 +90,8 @@ struct Seg {
     int tile;                  // linear tile index (m fastest), SCHED 1 flag index base
     int bz, mt, nt, kb0, nkb;  // mt = index of the CTA group's tile
     int mode;
-    int ntails;                // SCHED 1: segments of this tile after its head
+    int ntails;                // SCHED 1/2: segments of this tile after its head
+    int tstride;               // groups between consecutive segments of a split tile (SCHED 1: 1)
 };
 
 // Walks the segments (tile, k range) of one CTA group.  SCHED 0: units u = g, g+G, ...
@@ -90,8 +102,13 @@ struct SegIter {
     int u;
     __device__ SegIter(const TcParams& p, int g, int G) {
         u = g;
-        cur = (long long)g * p.total_iters / G;
-        end = (long long)(g + 1) * p.total_iters / G;
+        if (p.sched == 2) {  // the remainder unit of this group (if any): [g, g + 1)
+            cur = g;
+            end = g + 1;
+        } else {
+            cur = (long long)g * p.total_iters / G;
+            end = (long long)(g + 1) * p.total_iters / G;
+        }
     }
     __device__ bool next(const TcParams& p, int G, Seg& s) {
         int t;
@@ -110,6 +127,21 @@ struct SegIter {
             s.mode = EPI_STORE;
             s.ntails = 0;
             u += G;
+        } else if (p.sched == 2) {
+            // SCHED 2 remainder: R = tiles - dp_tiles tiles, each cut into S equal k-chunks;
+            // unit v = chunk * R + tile (chunk-major) goes to group v, so the groups working at
+            // the same time share few k-slices (their operand reads overlap in L2); chunk 0
+            // is the head, chunks 1..S-1 are tails parked by groups v + R, v + 2R, ...
+            const int R = p.rem_tiles, S = p.rem_chunks, v = (int)cur;
+            if (cur >= end || v >= R * S) return false;
+            cur = end;  // one remainder unit per group
+            const int c = v / R;
+            t = p.dp_tiles + v % R;
+            s.kb0 = (int)((long long)c * p.kblocks / S);
+            s.nkb = (int)((long long)(c + 1) * p.kblocks / S) - s.kb0;
+            s.mode = S == 1 ? EPI_STORE : (c == 0 ? EPI_HEAD : EPI_TAIL);
+            s.ntails = c == 0 ? S - 1 : 0;
+            s.tstride = R;
         } else {
             if (cur >= end) return false;
             const int tl = (int)(cur / p.kblocks);  // tile index within the streamed remainder
@@ -124,6 +156,7 @@ struct SegIter {
             // groups sharing this tile: g(i) = ceil((i+1) G / T) - 1 owns iteration i
             const long long T = p.total_iters, i0 = (long long)tl * p.kblocks, i1 = i0 + p.kblocks - 1;
             s.ntails = (int)(((i1 + 1) * G + T - 1) / T - ((i0 + 1) * G + T - 1) / T);
+            s.tstride = 1;
             cur += s.nkb;
         }
         s.tile = t;
@@ -135,12 +168,24 @@ struct SegIter {
     }
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// trace slots: 0 start, 1..4 epilogue segment j ready (acc_full), 5..8 segment j done,
+// 9 head flags seen, 10 end
+#define TC_TRACE(slot)                                                                   \
+    do {                                                                                 \
+        if (p.trace) p.trace[(size_t)blockIdx.x * 16 + (slot)] = gtimer();               \
+    } while (0)
+
 __device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 
 template <int BN, int BK, int STAGES, int TQ, int CG>
 __global__ void __launch_bounds__(192, 1)
     tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const TcParams p) {
+                        const __grid_constant__ CUtensorMap tmY, const TcParams p) {
     using Cfg = TcCfg<BN, BK, STAGES, CG>;
     constexpr int BM = Cfg::BM;
     constexpr bool CONV = TQ > 0;
@@ -153,9 +198,11 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* acc_full = bars + 2 * STAGES;       // [2] MMA -> epilogue
     uint64_t* acc_empty = bars + 2 * STAGES + 2;  // [2] epilogue -> MMA
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+    float* epi_smem = reinterpret_cast<float*>(base + STAGES * Cfg::STAGE_BYTES + 256);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? tc::cluster_ctarank() : 0u;
+    if (threadIdx.x == 0) TC_TRACE(0);
     const int group = blockIdx.x / CG, ngroups = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
@@ -279,7 +326,8 @@ __global__ void __launch_bounds__(192, 1)
     } else {  // ---- epilogue: TMEM -> registers -> global
         const int q = warp & 3;
         const int trow = q * 32 + lane;  // row of the 128-row sub-tile held by this thread
-        const bool vec_ok = (p.N % 4) == 0;
+        const bool vec_ok = (p.N % 4) == 0;  // TMA needs 16-byte global strides
+        int ebuf = 0;                        // staging boxes used so far by this warp
         int j = 0;
         SegIter si(p, group, ngroups);
         Seg w;
@@ -300,18 +348,33 @@ __global__ void __launch_bounds__(192, 1)
                 row_ok = row_ok && m < p.M;
                 orow = (long long)w.bz * p.M + m;
             }
+            // TMA-store box origin of this warp's 32 rows: dense (col, row, batch); conv
+            // (k, q, p, image) with the rows forming a (32 / TQ) x TQ pixel rectangle
+            int bx1 = 0, bx2 = 0, bx3 = 0;
+            if constexpr (CONV) {
+                constexpr int TQW = TQ < 32 ? TQ : 32;
+                bx1 = (mt % p.tiles_q) * TQ + ((q * 32) % TQ);
+                const int t = mt / p.tiles_q;
+                bx2 = (t % p.tiles_p) * TP + (q * 32) / TQ * (TQ / TQW);
+                bx3 = t / p.tiles_p;
+            } else {
+                bx1 = mt * BM + q * 32;
+                bx2 = w.bz;
+            }
             tc::mbar_wait(tc::smem_u32(&acc_full[a]), (uint32_t)(j >> 1) & 1u);
             tc::tc_fence_after();
+            if (warp == 2 && lane == 0 && j < 4) TC_TRACE(1 + j);
             const int slot = group * CG + (int)rank;  // this group's workspace slot (stream-K)
             if (w.mode == EPI_HEAD) {  // wait until every tail of this tile parked its partial
                 if (warp == 2 && lane == 0) {
                     for (int tl = 1; tl <= w.ntails; ++tl) {
-                        const unsigned* f = p.flags + (slot + tl * CG);
+                        const unsigned* f = p.flags + (slot + tl * w.tstride * CG);
                         unsigned v;
                         do {
                             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
                         } while (v == 0u);
                     }
+                    TC_TRACE(9);
                 }
                 epi_bar(1);
             }
@@ -334,10 +397,49 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                 for (int g = 0; g < CH / 16; ++g) {
                     const int n = n0 + c0 + g * 16;
+                    // the output through TMA stores (OOB rows / columns / pixels are clipped)
+                    if (w.mode != EPI_TAIL && vec_ok) {
+                        if (w.mode == EPI_HEAD && live) {
+                            for (int tl = 1; tl <= w.ntails; ++tl) {
+                                const float* pp = p.ws + (long long)(slot + tl * w.tstride * CG) * 128 * 256 +
+                                                  (long long)((c0 + g * 16) / 16) * (128 * 16) + trow * 16;
+#pragma unroll
+                                for (int v = 0; v < 4; ++v) {
+                                    const float4 x = __ldcg(reinterpret_cast<const float4*>(pp) + v);
+                                    r[g][4 * v] = __float_as_uint(__uint_as_float(r[g][4 * v]) + x.x);
+                                    r[g][4 * v + 1] = __float_as_uint(__uint_as_float(r[g][4 * v + 1]) + x.y);
+                                    r[g][4 * v + 2] = __float_as_uint(__uint_as_float(r[g][4 * v + 2]) + x.z);
+                                    r[g][4 * v + 3] = __float_as_uint(__uint_as_float(r[g][4 * v + 3]) + x.w);
+                                }
+                            }
+                        }
+                        float* eb = epi_smem + (q * 2 + (ebuf & 1)) * Cfg::EPI_BOX;
+                        if (lane == 0) tc::bulk_wait_read<1>();  // the store that last used this box has read it
+                        __syncwarp();
+#pragma unroll
+                        for (int v = 0; v < 4; ++v)
+                            *reinterpret_cast<uint4*>(eb + lane * 16 + 4 * v) =
+                                make_uint4(r[g][4 * v], r[g][4 * v + 1], r[g][4 * v + 2], r[g][4 * v + 3]);
+                        tc::fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            const uint32_t src = tc::smem_u32(eb);
+                            if constexpr (CONV) {
+                                if (red) tc::tma_red_add_4d(&tmY, src, n, bx1, bx2, bx3);
+                                else tc::tma_store_4d(&tmY, src, n, bx1, bx2, bx3);
+                            } else {
+                                if (red) tc::tma_red_add_3d(&tmY, src, n, bx1, bx2);
+                                else tc::tma_store_3d(&tmY, src, n, bx1, bx2);
+                            }
+                            tc::bulk_commit();
+                        }
+                        ++ebuf;
+                        continue;
+                    }
                     if (!live || n >= ncols) continue;
                     if (w.mode == EPI_HEAD) {  // add the tails' partials (same rows, same columns)
                         for (int tl = 1; tl <= w.ntails; ++tl) {
-                            const float* pp = p.ws + (long long)(slot + tl * CG) * 128 * 256 +
+                            const float* pp = p.ws + (long long)(slot + tl * w.tstride * CG) * 128 * 256 +
                                               (long long)((c0 + g * 16) / 16) * (128 * 16) + trow * 16;
 #pragma unroll
                             for (int v = 0; v < 4; ++v) {
@@ -375,6 +477,7 @@ __global__ void __launch_bounds__(192, 1)
                 if constexpr (CG == 2) tc::mbar_arrive_remote(tc::smem_u32(&acc_empty[a]), 0);
                 else tc::mbar_arrive(tc::smem_u32(&acc_empty[a]));
             }
+            if (warp == 2 && lane == 0 && j < 4) TC_TRACE(5 + j);
             if (w.mode == EPI_TAIL) {  // publish the parked partial (flag = 1)
                 epi_bar(2);
                 if (warp == 2 && lane == 0) {
@@ -384,14 +487,17 @@ __global__ void __launch_bounds__(192, 1)
             } else if (w.mode == EPI_HEAD) {  // partials consumed: re-arm the tails' flags (0)
                 epi_bar(2);
                 if (warp == 2 && lane == 0) {
-                    for (int tl = 1; tl <= w.ntails; ++tl) p.flags[slot + tl * CG] = 0u;
+                    for (int tl = 1; tl <= w.ntails; ++tl) p.flags[slot + tl * w.tstride * CG] = 0u;
                 }
             }
         }
+        if (lane == 0) tc::bulk_wait_all();  // this warp's TMA stores are complete
+        __syncwarp();
     }
     tc::tc_fence_before();
     if constexpr (CG == 2) tc::cluster_sync();
     else __syncthreads();
+    if (threadIdx.x == 0) TC_TRACE(10);
     if (warp == 1) {
         tc::tc_fence_after();
         if constexpr (CG == 2) tc::tmem_dealloc_cg2<Cfg::TMEM_COLS>(tmem);
@@ -422,6 +528,17 @@ static bool encode(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* 
     if (!enc) return false;
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// fp32 tensor (the output Y), no swizzle: a box lands row-major in shared memory
+static bool encode_f32(CUtensorMap* m, void* ptr, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                       const cuuint32_t* box, const cuuint32_t* es) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, ptr, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -510,6 +627,27 @@ cudaError_t tc_launch(const LaunchCtx& c) {
         p.m_tiles = (int)((s.M + Cfg::BM - 1) / Cfg::BM);
         p.batch = (int)s.batch;
     }
+    // Y (fp32) for the TMA-store epilogue: one box = one epilogue warp's 32 rows x 16 columns
+    CUtensorMap ty;
+    std::memset(&ty, 0, sizeof(ty));
+    if (s.N % 4 == 0) {
+        bool ok;
+        if constexpr (CONV) {
+            constexpr int TQW = TQ < 32 ? TQ : 32;
+            cuuint64_t yd[4] = {(cuuint64_t)s.k, (cuuint64_t)s.q, (cuuint64_t)s.p, (cuuint64_t)s.n};
+            cuuint64_t ys[3] = {(cuuint64_t)s.k * 4, (cuuint64_t)(s.q * s.k * 4), (cuuint64_t)(s.p * s.q * s.k * 4)};
+            cuuint32_t yb[4] = {16, (cuuint32_t)TQW, (cuuint32_t)(32 / TQW), 1};
+            cuuint32_t ye[4] = {1, 1, 1, 1};
+            ok = encode_f32(&ty, c.y, 4, yd, ys, yb, ye);
+        } else {
+            cuuint64_t yd[3] = {(cuuint64_t)s.N, (cuuint64_t)s.M, (cuuint64_t)s.batch};
+            cuuint64_t ys[2] = {(cuuint64_t)s.N * 4, (cuuint64_t)(s.M * s.N * 4)};
+            cuuint32_t yb[3] = {16, 32, 1};
+            cuuint32_t ye[3] = {1, 1, 1};
+            ok = encode_f32(&ty, c.y, 3, yd, ys, yb, ye);
+        }
+        if (!ok) return cudaErrorInvalidValue;
+    }
     p.mp_tiles = (p.m_tiles + CG - 1) / CG;
     const long long tiles = (long long)p.batch * p.mp_tiles * p.n_tiles;
     const long long units = tiles * c.split;
@@ -532,10 +670,15 @@ cudaError_t tc_launch(const LaunchCtx& c) {
         if (!stream_k_scratch(&p.flags, &p.ws)) return cudaErrorMemoryAllocation;
         if (groups > p.total_iters) groups = p.total_iters;
         if (groups * CG > kStreamKSlots) groups = kStreamKSlots / CG;
-        if (c.sched == 2) {  // whole waves tile by tile, only the remainder streamed (groups with
-                             // an empty share of the remainder simply stop after their waves)
+        if (c.sched == 2) {  // whole waves tile by tile; the remainder tiles cut into equal k-chunks,
+                             // one chunk per group (groups without one stop after their waves)
             p.dp_tiles = (int)((tiles / groups) * groups);
-            p.total_iters = (tiles - p.dp_tiles) * p.kblocks;
+            p.rem_tiles = (int)(tiles - p.dp_tiles);
+            long long S = p.rem_tiles ? groups / p.rem_tiles : 1;
+            if (S < 1) S = 1;
+            if (S > p.kblocks) S = p.kblocks;
+            p.rem_chunks = (int)S;
+            p.total_iters = (long long)p.rem_tiles * p.kblocks;
         }
     } else if (groups > units) {
         groups = units;
@@ -553,13 +696,34 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+    static const bool tracing = std::getenv("DB200_TC_TRACE") != nullptr;
+    static unsigned long long* trace_buf = nullptr;
+    if (tracing && !trace_buf && cudaMalloc(&trace_buf, 4096 * 16 * sizeof(unsigned long long)) != cudaSuccess)
+        trace_buf = nullptr;
+    p.trace = tracing ? trace_buf : nullptr;
+    if (p.trace) cudaMemsetAsync(p.trace, 0, (size_t)cfg.gridDim.x * 16 * sizeof(unsigned long long), c.stream);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, ty, p);
     count_launches(1);
+    if (p.trace && e == cudaSuccess) {  // debug: per-CTA timeline in microseconds from the earliest start
+        std::vector<unsigned long long> h((size_t)cfg.gridDim.x * 16);
+        cudaStreamSynchronize(c.stream);
+        cudaMemcpy(h.data(), p.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+        unsigned long long t0 = ~0ull;
+        for (unsigned i = 0; i < cfg.gridDim.x; ++i) t0 = std::min(t0, h[i * 16]);
+        std::fprintf(stderr, "TC_TRACE sched %d groups %lld tiles %lld dp %d rem %d chunks %d\n", p.sched, groups,
+                     tiles, p.dp_tiles, p.rem_tiles, p.rem_chunks);
+        for (unsigned i = 0; i < cfg.gridDim.x; i += CG) {
+            std::fprintf(stderr, "cta %3u:", i);
+            for (int k = 0; k < 11; ++k)
+                std::fprintf(stderr, " %7.2f", h[i * 16 + k] ? (h[i * 16 + k] - t0) * 1e-3 : -1.0);
+            std::fprintf(stderr, "\n");
+        }
+    }
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 constexpr bool tc_static_ok(int BN, int BK, int STAGES, int CG) {
-    return 1024 + (size_t)STAGES * (128 + BN / CG) * BK * 2 + 256 <= 227 * 1024;
+    return 1024 + (size_t)STAGES * (128 + BN / CG) * BK * 2 + 256 + kTcEpiBytes <= 227 * 1024;
 }
 
 template <int BN, int BK, int STAGES, int TQ, int CG>

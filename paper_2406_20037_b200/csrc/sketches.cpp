@@ -26,7 +26,7 @@ static std::vector<SketchDesc> build_catalogue() {
     // split-K (runtime).
     // BM = 256 is the CTA-pair schedule (cta_group::2, UMMA M = 256 over two SMs);
     // SCHED 0 = persistent tile loop (+ split-K), 1 = stream-K (equal share of all k-blocks),
-    // 2 = whole waves tile by tile + the remainder tiles stream-K.
+    // 2 = whole waves tile by tile + the remainder tiles cut into k-chunks, one per group.
     const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED"};
     const std::vector<std::vector<int32_t>> tc_vals = {{128, 256}, {64, 128, 256}, {64, 128}, {2, 3, 4, 6},
                                                        {1, 2, 4},  {0, 1, 2}};
@@ -152,7 +152,8 @@ static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
     }
     if (bn > 256 || (bm != 128 && bm != 256)) return false;
     const int cg = bm / 128;  // CTAs per tile: each stages 128 rows of A and bn/cg rows of B
-    const int64_t smem = (int64_t)stages * (128 + bn / cg) * bk * 2 + 1024 /*align*/ + 256 /*barriers*/;
+    const int64_t smem = (int64_t)stages * (128 + bn / cg) * bk * 2 + 1024 /*align*/ + 256 /*barriers*/ +
+                         kTcEpiBytes /*epilogue staging*/;
     if (smem > 227 * 1024) return false;
     if (split > ktiles) return false;
     if ((int64_t)split * sh.batch > 65535) return false;

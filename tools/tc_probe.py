@@ -15,6 +15,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mnk", nargs="+", default=["8192,8192,8192", "8192,768,3072", "8192,3072,768"])
+    ap.add_argument("--dpansor", type=int, default=120, help="evolve trials before Droplet (0: skip)")
     ap.add_argument("--configs", nargs="*", default=["256,256,64,4,1,0", "256,256,128,3,1,0", "256,128,128,4,1,0",
                                                       "128,256,64,6,1,0", "256,256,64,6,1,1"])
     a = ap.parse_args()
@@ -37,10 +38,11 @@ def main():
         fl = 2.0 * m * n * k
         for p, r in zip(pts, t.measure(pts)):
             print(f"{mnk:16s} {t.values(p)} {r.status:5s} {r.cost_ns / 1e3:9.1f} us {fl / r.cost_ns / 1e3:7.1f} TFLOP/s")
-        t.evolve(120)
-        rep = t.droplet(t.best().point, 60)
-        print(f"{mnk:16s} DPAnsor best {t.values(rep['best'])} {rep['best_cost'] / 1e3:9.1f} us "
-              f"{fl / rep['best_cost'] / 1e3:7.1f} TFLOP/s")
+        if a.dpansor > 0:
+            t.evolve(a.dpansor)
+            rep = t.droplet(t.best().point, 60)
+            print(f"{mnk:16s} DPAnsor best {t.values(rep['best'])} {rep['best_cost'] / 1e3:9.1f} us "
+                  f"{fl / rep['best_cost'] / 1e3:7.1f} TFLOP/s")
         # torch (cuBLAS) for context
         xa, wa = x[0], w[0]
         for _ in range(3):
