@@ -53,7 +53,7 @@ static tuner_status cuda_fail(cudaError_t e, const char* what) {
 
 // launcher + runtime knobs of a point
 struct RuntimeKnobs {
-    int split = 1, vec = 1, stages = 1, sched = 0;
+    int split = 1, vec = 1, stages = 1, sched = 0, raster = 0;
     int dims[3] = {1, 1, 1};
 };
 static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
@@ -69,13 +69,15 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
             rk.stages = v[6];
             rk.split = v[7];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[4]));
-        case SK_TC_GEMM_BF16:
+        case SK_TC_GEMM_BF16:  // BM, BN, BK, STAGES, SPLIT_K, SCHED, RASTER
             rk.split = v[4];
             rk.sched = v[5];
+            rk.raster = v[6];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], 0));
-        case SK_TC_IGEMM_CONV_BF16:
+        case SK_TC_IGEMM_CONV_BF16:  // BM, BN, BK, STAGES, SPLIT_K, TILE_Q, SCHED, RASTER
             rk.split = v[4];
             rk.sched = v[6];
+            rk.raster = v[7];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[5]));
         case SK_SIMT_DWCONV_F32:
         case SK_SIMT_DWCONV_BF16:  // VEC, CT, TQ, QT, PT, TP, ALG
@@ -226,6 +228,7 @@ struct GpuMeasurer : Measurer {
             ctx.stages = rk[j].stages;
             ctx.sched = rk[j].sched;
             for (int d = 0; d < 3; ++d) ctx.dims[d] = rk[j].dims[d];
+            ctx.raster = rk[j].raster;
         };
 
         // ---- phase 1: verification run (also the first, untimed-for-cost launch)
@@ -387,6 +390,7 @@ tuner_status gpu_kernel_run(const Tuner* t, const Pt& p, const tuner_buffers* bu
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     LaunchCtx ctx{&t->info, buf->x, buf->w, buf->y, rk.split, rk.vec, rk.stages, rk.sched, (cudaStream_t)stream, nsm};
     for (int d = 0; d < 3; ++d) ctx.dims[d] = rk.dims[d];
+    ctx.raster = rk.raster;
     CU(fn(ctx));
     return TUNER_OK;
 }

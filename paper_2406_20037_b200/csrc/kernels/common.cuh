@@ -21,6 +21,7 @@ struct LaunchCtx {
     cudaStream_t stream;
     int num_sms;
     int dims[3] = {1, 1, 1};  // runtime thread-block shape knobs (depthwise: CT, QT, PT)
+    int raster = 0;           // runtime tile order (tcgen05): 0 = M fastest, 1 = N fastest
 };
 
 typedef cudaError_t (*LaunchFn)(const LaunchCtx&);

@@ -67,7 +67,8 @@ struct TcParams {
     int m_tiles;                  // 128-row sub-tiles per batch (conv: images x pixel tiles)
     int mp_tiles, n_tiles, batch;  // tiles of the CTA group (CG sub-tiles each)
     int units;                    // SCHED 0: batch * mp_tiles * n_tiles * split
-    int sched;                    // 0 = tiles (+ split-K), 1 = stream-K, 2 = full waves by tile + stream-K rest
+    int sched;                    // 0 = tiles (+ split-K), 1 = stream-K, 2 = full waves by tile + k-chunked rest
+    int raster;                   // tile order: 0 = M fastest, 1 = N fastest
     int dp_tiles;                 // SCHED 2: tiles handled whole (a multiple of the group count)
     int rem_tiles, rem_chunks;    // SCHED 2: remainder tiles and k-chunks per remainder tile
     long long total_iters;        // SCHED 1/2: streamed k-block iterations (tiles - dp_tiles) * kblocks
@@ -160,10 +161,16 @@ struct SegIter {
             cur += s.nkb;
         }
         s.tile = t;
-        s.mt = t % p.mp_tiles;  // m fastest: concurrent CTAs share the B (weight) tile in L2
-        t /= p.mp_tiles;
-        s.nt = t % p.n_tiles;
-        s.bz = t / p.n_tiles;
+        if (p.raster == 0) {  // m fastest: concurrent CTAs share the B (weight) panel in L2
+            s.mt = t % p.mp_tiles;
+            t /= p.mp_tiles;
+            s.nt = t % p.n_tiles;
+        } else {  // n fastest: concurrent CTAs share the A panel
+            s.nt = t % p.n_tiles;
+            t /= p.n_tiles;
+            s.mt = t % p.mp_tiles;
+        }
+        s.bz = t / (p.raster == 0 ? p.n_tiles : p.mp_tiles);
         return true;
     }
 };
@@ -394,25 +401,34 @@ __global__ void __launch_bounds__(192, 1)
                 for (int g = 0; g < CH / 16; ++g)
                     tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + c0 + g * 16), r[g]);
                 tc::tmem_ld_wait();
+                if (w.mode == EPI_HEAD && live) {
+                    // add the tails' parked partials (same rows, same columns): all of a tail's
+                    // loads for this chunk are issued before any add, so they overlap in flight
+                    for (int tl = 1; tl <= w.ntails; ++tl) {
+                        const float4* pp = reinterpret_cast<const float4*>(
+                            p.ws + (long long)(slot + tl * w.tstride * CG) * 128 * 256 +
+                            (long long)(c0 / 16) * (128 * 16) + trow * 16);
+                        float4 x[CH / 16][4];
+#pragma unroll
+                        for (int g = 0; g < CH / 16; ++g)
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) x[g][v] = __ldcg(pp + g * (128 * 16 / 4) + v);
+#pragma unroll
+                        for (int g = 0; g < CH / 16; ++g)
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                r[g][4 * v] = __float_as_uint(__uint_as_float(r[g][4 * v]) + x[g][v].x);
+                                r[g][4 * v + 1] = __float_as_uint(__uint_as_float(r[g][4 * v + 1]) + x[g][v].y);
+                                r[g][4 * v + 2] = __float_as_uint(__uint_as_float(r[g][4 * v + 2]) + x[g][v].z);
+                                r[g][4 * v + 3] = __float_as_uint(__uint_as_float(r[g][4 * v + 3]) + x[g][v].w);
+                            }
+                    }
+                }
 #pragma unroll
                 for (int g = 0; g < CH / 16; ++g) {
                     const int n = n0 + c0 + g * 16;
                     // the output through TMA stores (OOB rows / columns / pixels are clipped)
                     if (w.mode != EPI_TAIL && vec_ok) {
-                        if (w.mode == EPI_HEAD && live) {
-                            for (int tl = 1; tl <= w.ntails; ++tl) {
-                                const float* pp = p.ws + (long long)(slot + tl * w.tstride * CG) * 128 * 256 +
-                                                  (long long)((c0 + g * 16) / 16) * (128 * 16) + trow * 16;
-#pragma unroll
-                                for (int v = 0; v < 4; ++v) {
-                                    const float4 x = __ldcg(reinterpret_cast<const float4*>(pp) + v);
-                                    r[g][4 * v] = __float_as_uint(__uint_as_float(r[g][4 * v]) + x.x);
-                                    r[g][4 * v + 1] = __float_as_uint(__uint_as_float(r[g][4 * v + 1]) + x.y);
-                                    r[g][4 * v + 2] = __float_as_uint(__uint_as_float(r[g][4 * v + 2]) + x.z);
-                                    r[g][4 * v + 3] = __float_as_uint(__uint_as_float(r[g][4 * v + 3]) + x.w);
-                                }
-                            }
-                        }
                         float* eb = epi_smem + (q * 2 + (ebuf & 1)) * Cfg::EPI_BOX;
                         if (lane == 0) tc::bulk_wait_read<1>();  // the store that last used this box has read it
                         __syncwarp();
@@ -437,20 +453,6 @@ __global__ void __launch_bounds__(192, 1)
                         continue;
                     }
                     if (!live || n >= ncols) continue;
-                    if (w.mode == EPI_HEAD) {  // add the tails' partials (same rows, same columns)
-                        for (int tl = 1; tl <= w.ntails; ++tl) {
-                            const float* pp = p.ws + (long long)(slot + tl * w.tstride * CG) * 128 * 256 +
-                                              (long long)((c0 + g * 16) / 16) * (128 * 16) + trow * 16;
-#pragma unroll
-                            for (int v = 0; v < 4; ++v) {
-                                const float4 x = __ldcg(reinterpret_cast<const float4*>(pp) + v);
-                                r[g][4 * v] = __float_as_uint(__uint_as_float(r[g][4 * v]) + x.x);
-                                r[g][4 * v + 1] = __float_as_uint(__uint_as_float(r[g][4 * v + 1]) + x.y);
-                                r[g][4 * v + 2] = __float_as_uint(__uint_as_float(r[g][4 * v + 2]) + x.z);
-                                r[g][4 * v + 3] = __float_as_uint(__uint_as_float(r[g][4 * v + 3]) + x.w);
-                            }
-                        }
-                    }
                     if ((vec_ok || w.mode == EPI_TAIL) && n + 16 <= ncols) {
                         float* dst = w.mode == EPI_TAIL ? crow + (long long)(n / 16) * (128 * 16) : crow + n;
 #pragma unroll
@@ -654,6 +656,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     if (units >= (1ll << 31)) return cudaErrorInvalidValue;
     p.units = (int)units;
     p.sched = c.sched;
+    p.raster = c.raster;
     p.total_iters = tiles * p.kblocks;
     if (c.split > 1) {
         cudaError_t e = cudaMemsetAsync(c.y, 0, (size_t)s.y_elems * sizeof(float), c.stream);

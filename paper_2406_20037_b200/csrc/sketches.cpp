@@ -27,16 +27,19 @@ static std::vector<SketchDesc> build_catalogue() {
     // BM = 256 is the CTA-pair schedule (cta_group::2, UMMA M = 256 over two SMs);
     // SCHED 0 = persistent tile loop (+ split-K), 1 = stream-K (equal share of all k-blocks),
     // 2 = whole waves tile by tile + the remainder tiles cut into k-chunks, one per group.
-    const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED"};
+    // RASTER (runtime): the order tiles are handed to the persistent CTAs, 0 = M fastest
+    // (concurrent CTAs share the B panel), 1 = N fastest (they share the A panel).
+    const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER"};
     const std::vector<std::vector<int32_t>> tc_vals = {{128, 256}, {64, 128, 256}, {64, 128}, {2, 3, 4, 6},
-                                                       {1, 2, 4},  {0, 1, 2}};
+                                                       {1, 2, 4},  {0, 1, 2},       {0, 1}};
     c.push_back({SK_TC_GEMM_BF16, "tc_gemm_bf16", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL), TUNER_BF16,
                  tc_names, tc_vals});
     // implicit-GEMM conv: the 128-row M tile is a (128/TILE_Q) x TILE_Q rectangle of output pixels
-    const std::vector<const char*> tcc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "TILE_Q", "SCHED"};
-    std::vector<std::vector<int32_t>> tcc_vals(tc_vals.begin(), tc_vals.end() - 1);
+    const std::vector<const char*> tcc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "TILE_Q", "SCHED", "RASTER"};
+    std::vector<std::vector<int32_t>> tcc_vals(tc_vals.begin(), tc_vals.end() - 2);
     tcc_vals.push_back({8, 16, 32});
     tcc_vals.push_back({0, 1, 2});
+    tcc_vals.push_back({0, 1});
     c.push_back({SK_TC_IGEMM_CONV_BF16, "tc_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tcc_names,
                  tcc_vals});
     // the SIMT implicit-GEMM sketch on bf16 inputs (widened to fp32 at staging, fp32

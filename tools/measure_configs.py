@@ -44,6 +44,7 @@ def main():
     pts = []
     for c in a.configs:
         vals = [int(v) for v in c.split(",")]
+        vals += [space[d][0] for d in range(len(vals), len(space))]  # omitted trailing knobs: first value
         pts.append((sk, tuple(space[d].index(v) for d, v in enumerate(vals))))
     fl = layer_flops(L)
     for p, r in zip(pts, t.measure(pts)):

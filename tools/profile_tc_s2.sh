@@ -11,6 +11,7 @@ sp = sketch_space(2)
 x = torch.randn(1, m, k, device="cuda").to(torch.bfloat16); w = torch.randn(1, n, k, device="cuda").to(torch.bfloat16)
 y = torch.empty(1, m, n, device="cuda")
 t = Tuner("dense", {"m": m, "n": n, "k": k}, dtype="bf16", spaces=[(2, sp)], x=x, w=w, y=y, verify=False)
+vals += [sp[d][0] for d in range(len(vals), len(sp))]
 p = (2, tuple(sp[d].index(v) for d, v in enumerate(vals)))
 for _ in range(4): t.run(p, x, w, y)
 torch.cuda.synchronize()

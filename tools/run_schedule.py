@@ -48,6 +48,7 @@ def main():
     sk = a.sketch if a.sketch is not None else sketches(L["op"], a.dtype)[0]
     vals = [int(v) for v in a.values.split(",")]
     space = sketch_space(sk)
+    vals += [space[d][0] for d in range(len(vals), len(space))]  # omitted trailing knobs: first value
     idx = tuple(space[d].index(v) for d, v in enumerate(vals))
     t = Tuner(L["op"], shape, dtype=a.dtype, spaces=[(sk, space)], x=xd, w=wd, y=y, verify=a.measure,
               repeats=3, warmup=1)

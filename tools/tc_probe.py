@@ -32,6 +32,7 @@ def main():
         pts = []
         for c in a.configs:
             vals = [int(v) for v in c.split(",")]
+            vals += [sp[d][0] for d in range(len(vals), len(sp))]  # omitted trailing knobs: first value
             p = (2, tuple(sp[d].index(v) for d, v in enumerate(vals)))
             if t.valid(p):
                 pts.append(p)
