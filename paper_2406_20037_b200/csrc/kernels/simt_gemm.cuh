@@ -66,6 +66,17 @@ __device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {  // 4 x bf16 = o
                        __uint_as_float(u.y & 0xFFFF0000u));
 }
 
+// c + a * (b0, b1) as two RN fused multiply-adds in one FFMA2 (fma.rn.f32x2)
+__device__ __forceinline__ float2 ffma2(float a, float b0, float b1, float2 c) {
+    const float2 av = make_float2(a, a), bv = make_float2(b0, b1);
+    float2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+        : "l"(*reinterpret_cast<const unsigned long long*>(&av)), "l"(*reinterpret_cast<const unsigned long long*>(&bv)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+    return r;
+}
+
 // Row r of a thread's TT-row register tile -> row inside the block tile.
 // TT <= 4: contiguous; TT = 8: two 4-row groups BM/2 apart (conflict-free LDS.128).
 template <int BMN, int TT>
@@ -131,11 +142,14 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
         __syncthreads();
     }
 
-    float acc[TT][TT];
+    // accumulators as column pairs: one FFMA2 (fma.rn.f32x2, sm_100) updates two of them with
+    // a broadcast A value -- the same two RN fused multiply-adds, half the issue slots
+    float2 acc[TT][TT / 2];
 #pragma unroll
     for (int i = 0; i < TT; ++i)
 #pragma unroll
-        for (int j = 0; j < TT; ++j) acc[i][j] = 0.f;
+        for (int j = 0; j < TT / 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    auto accv = [&](int i, int j) -> float { return (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x; };
 
     // staging registers: each slot holds 4 consecutive k of one row
     float4 ra[Cfg::SA], rb[Cfg::SB];
@@ -292,7 +306,7 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
 #pragma unroll
             for (int i = 0; i < TT; ++i)
 #pragma unroll
-                for (int j = 0; j < TT; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < TT / 2; ++j) acc[i][j] = ffma2(a[i], b[2 * j], b[2 * j + 1], acc[i][j]);
         }
     };
 
@@ -333,19 +347,19 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
             constexpr int W = TT < 4 ? TT : 4;
             const int n = n0 + tile_row<BN, TT>(tx, W * g);
             if (W == 4 && n + 3 < p.N && (p.N % 4) == 0) {
-                float4 v = make_float4(acc[i][4 * g], acc[i][4 * g + 1], acc[i][4 * g + 2], acc[i][4 * g + 3]);
+                float4 v = make_float4(accv(i, 4 * g), accv(i, 4 * g + 1), accv(i, 4 * g + 2), accv(i, 4 * g + 3));
                 if (atomic) atomicAdd(reinterpret_cast<float4*>(crow + n), v);
                 else *reinterpret_cast<float4*>(crow + n) = v;
             } else if (W == 2 && n + 1 < p.N && (p.N % 2) == 0) {
-                float2 v = make_float2(acc[i][0], acc[i][1]);
+                float2 v = make_float2(accv(i, 0), accv(i, 1));
                 if (atomic) atomicAdd(reinterpret_cast<float2*>(crow + n), v);
                 else *reinterpret_cast<float2*>(crow + n) = v;
             } else {
 #pragma unroll
                 for (int j = 0; j < W; ++j) {
                     if (n + j < p.N) {
-                        if (atomic) atomicAdd(crow + n + j, acc[i][W * g + j]);
-                        else crow[n + j] = acc[i][W * g + j];
+                        if (atomic) atomicAdd(crow + n + j, accv(i, W * g + j));
+                        else crow[n + j] = accv(i, W * g + j);
                     }
                 }
             }
