@@ -205,18 +205,32 @@ __global__ void __launch_bounds__(512) dwconv_win_kernel(const DwParams p) {
             for (int e = 0; e < VEC; ++e) acc[a][b][e] = 0.f;
 
     const int h0 = p0 * SH - p.ph, w0 = q0 * SH - p.pw;
+    // column offsets and bounds are the same for every input row
+    int coff[NC];
+    bool cok[NC];
 #pragma unroll
-    for (int i = 0; i < NR; ++i) {
+    for (int j = 0; j < NC; ++j) {
+        coff[j] = (w0 + j) * p.C;
+        cok[j] = (unsigned)(w0 + j) < (unsigned)p.W;
+    }
+    // two input rows in flight: row i + 1 is loaded while row i feeds the FMAs
+    float xr[2][NC][VEC];
+    auto load_row = [&](int i, float (&dst)[NC][VEC]) {
         const int h = h0 + i;
         const bool hok = (unsigned)h < (unsigned)p.H;
-        float xr[NC][VEC];
+        const TIn* rowp = X + (long long)h * p.W * p.C;
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
-            const int w = w0 + j;
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) xr[j][e] = 0.f;
-            if (hok && (unsigned)w < (unsigned)p.W) Vec<TIn, VEC>::load(X + ((long long)h * p.W + w) * p.C, xr[j]);
+            for (int e = 0; e < VEC; ++e) dst[j][e] = 0.f;
+            if (hok && cok[j]) Vec<TIn, VEC>::load(rowp + coff[j], dst[j]);
         }
+    };
+    load_row(0, xr[0]);
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+        if (i + 1 < NR) load_row(i + 1, xr[(i + 1) & 1]);
+        const float(&cur)[NC][VEC] = xr[i & 1];
 #pragma unroll
         for (int a = 0; a < TP; ++a) {
             const int r = i - a * SH;  // compile-time after unrolling
@@ -226,7 +240,7 @@ __global__ void __launch_bounds__(512) dwconv_win_kernel(const DwParams p) {
 #pragma unroll
                 for (int s = 0; s < KS; ++s)
 #pragma unroll
-                    for (int e = 0; e < VEC; ++e) acc[a][b][e] = fmaf(xr[b * SH + s][e], wr[r * KS + s][e], acc[a][b][e]);
+                    for (int e = 0; e < VEC; ++e) acc[a][b][e] = fmaf(cur[b * SH + s][e], wr[r * KS + s][e], acc[a][b][e]);
         }
     }
 #pragma unroll

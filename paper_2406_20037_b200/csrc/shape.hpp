@@ -25,10 +25,10 @@ inline size_t dwconv_smem_bytes(int rs, int ctv, int win) { return (size_t)4 * (
 // tcgen05 sketches: shared memory of the epilogue TMA-store staging (4 warps x 2 boxes x 32 x 16 fp32)
 constexpr int kTcEpiBytes = 4 * 2 * 32 * 16 * 4;
 
-// depthwise register-window schedule (ALG 0): taps + one input row segment +
-// accumulators must fit the register budget (fp32 values per thread)
+// depthwise register-window schedule (ALG 0): taps + two input row segments (one in
+// flight) + accumulators must fit the register budget (fp32 values per thread)
 constexpr bool dw_win_fits(int vec, int tq, int tp, int ks, int sh) {
-    return (ks * ks + (tq - 1) * sh + ks + tp * tq) * vec <= 96;
+    return (ks * ks + 2 * ((tq - 1) * sh + ks) + tp * tq) * vec + ((tq - 1) * sh + ks) <= 90;
 }
 
 struct ShapeInfo {  // derived GEMM view of the problem (depthwise: M = n*p*q, N = c, K = r*s)
