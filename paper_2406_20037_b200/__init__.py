@@ -13,3 +13,5 @@ SK_TC_IGEMM_CONV_BF16 = 3
 SK_SIMT_IGEMM_CONV_BF16 = 4
 SK_SIMT_DWCONV_F32 = 5
 SK_SIMT_DWCONV_BF16 = 6
+SK_SIMT_PIPE_GEMM_F32 = 7
+SK_SIMT_PIPE_CONV_F32 = 8

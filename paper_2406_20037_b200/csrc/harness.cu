@@ -65,6 +65,8 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
         case SK_SIMT_GEMM_F32:
         case SK_SIMT_IGEMM_CONV_F32:
         case SK_SIMT_IGEMM_CONV_BF16:
+        case SK_SIMT_PIPE_GEMM_F32:  // BM, BN, BK, TT, KW | VEC, STAGES, SPLIT_K
+        case SK_SIMT_PIPE_CONV_F32:
             rk.vec = v[5];
             rk.stages = v[6];
             rk.split = v[7];

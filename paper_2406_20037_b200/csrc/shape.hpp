@@ -15,7 +15,9 @@ enum SketchId : int32_t {
     SK_SIMT_IGEMM_CONV_BF16 = 4,
     SK_SIMT_DWCONV_F32 = 5,
     SK_SIMT_DWCONV_BF16 = 6,
-    SK_COUNT = 7
+    SK_SIMT_PIPE_GEMM_F32 = 7,
+    SK_SIMT_PIPE_CONV_F32 = 8,
+    SK_COUNT = 9
 };
 
 // depthwise sketch: shared-memory bytes of a CTA (filters [R*S][ctv] + input window
@@ -30,6 +32,16 @@ constexpr int kTcEpiBytes = 4 * 2 * 32 * 16 * 4;
 constexpr bool dw_win_fits(int vec, int tq, int tp, int ks, int sh) {
     return (ks * ks + 2 * ((tq - 1) * sh + ks) + tp * tq) * vec + ((tq - 1) * sh + ks) <= 90;
 }
+
+// cp.async multistage SIMT sketches: shared-memory bytes of a launch (ring of STAGES
+// [BM+BN][BK+4] fp32 tiles, or the KW-group reduction tile if larger, + the conv k table)
+inline size_t pipe_smem_bytes(int bm, int bn, int bk, int kw, int stages, bool conv, int kspan, int vw) {
+    const size_t pipe = (size_t)stages * (bm + bn) * (bk + 4) * 4;
+    const size_t red = kw > 1 ? (size_t)kw * bm * bn * 4 : 0;
+    const size_t ktab = conv ? (size_t)((kspan + vw - 1) / vw) * 8 : 0;
+    return (pipe > red ? pipe : red) + ktab;
+}
+constexpr int kPipeMaxSlots = 8;  // cp.async slots per thread per operand
 
 struct ShapeInfo {  // derived GEMM view of the problem (depthwise: M = n*p*q, N = c, K = r*s)
     int32_t op, dtype;

@@ -21,6 +21,16 @@ static std::vector<SketchDesc> build_catalogue() {
                  TUNER_F32, simt_names, simt_vals});
     c.push_back({SK_SIMT_IGEMM_CONV_F32, "simt_igemm_conv_f32", 1 << TUNER_OP_CONV2D, TUNER_F32, simt_names,
                  simt_vals});
+    // cp.async multistage SIMT fp32 family (kernels/simt_pipe.cuh): STAGES-deep cp.async
+    // ring with zero-fill gathers, KW warp groups slicing each staged k-tile (summed through
+    // shared memory), k-parity FFMA2 accumulators; VEC = cp.async width, SPLIT_K as above.
+    const std::vector<const char*> pipe_names = {"BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K"};
+    const std::vector<std::vector<int32_t>> pipe_vals = {{32, 64, 128}, {32, 64, 128}, {8, 16, 32}, {2, 4},
+                                                         {1, 2, 4},     {1, 4},        {2, 3, 4, 6}, {1, 2, 4, 8, 16}};
+    c.push_back({SK_SIMT_PIPE_GEMM_F32, "simt_pipe_gemm_f32", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL),
+                 TUNER_F32, pipe_names, pipe_vals});
+    c.push_back({SK_SIMT_PIPE_CONV_F32, "simt_pipe_conv_f32", 1 << TUNER_OP_CONV2D, TUNER_F32, pipe_names,
+                 pipe_vals});
     // tcgen05 bf16 GEMM family: UMMA tile BM x BN (accumulator in TMEM), K step
     // BK staged by TMA with 128-byte swizzle, STAGES-deep mbarrier pipeline,
     // split-K (runtime).
@@ -135,6 +145,25 @@ static bool simt_valid(const ShapeInfo& sh, const int32_t* v) {
     return true;
 }
 
+static bool pipe_valid(const ShapeInfo& sh, const int32_t* v) {
+    const int bm = v[0], bn = v[1], bk = v[2], tt = v[3], kw = v[4], vec = v[5], stages = v[6], split = v[7];
+    const bool conv = sh.op == TUNER_OP_CONV2D;
+    if (tt > bm || tt > bn) return false;
+    const int gt = (bm / tt) * (bn / tt), threads = gt * kw;
+    if (gt < 32 || threads > 1024 || bk % (4 * kw)) return false;
+    if (vec == 4 && (conv ? (sh.c % 4) : (sh.K % 4)) != 0) return false;  // 16-byte cp.async inside one tap / row
+    const int chunks = (bm > bn ? bm : bn) * (bk / vec);
+    if ((chunks + threads - 1) / threads > kPipeMaxSlots) return false;  // cp.async slots per thread
+    const int64_t ktiles = (sh.K + bk - 1) / bk;
+    if (split > ktiles) return false;
+    const int64_t kspan = ((ktiles + split - 1) / split) * bk;
+    if (pipe_smem_bytes(bm, bn, bk, kw, stages, conv, (int)kspan, vec) > 227 * 1024) return false;
+    const int64_t ntiles = (sh.N + bn - 1) / bn;
+    if (ntiles > 65535 || (int64_t)split * sh.batch > 65535) return false;
+    if (conv && (sh.r - 1) * sh.dh >= 32767) return false;  // tap offsets packed in 16 bits
+    return true;
+}
+
 static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
     const int bm = v[0], bn = v[1], bk = v[2], stages = v[3], split = v[4];
     const int sched = sh.op == TUNER_OP_CONV2D ? v[6] : v[5];
@@ -191,6 +220,8 @@ bool sketch_valid(int32_t id, const ShapeInfo& sh, const int32_t* v) {
         case SK_SIMT_GEMM_F32:
         case SK_SIMT_IGEMM_CONV_F32:
         case SK_SIMT_IGEMM_CONV_BF16: return simt_valid(sh, v);
+        case SK_SIMT_PIPE_GEMM_F32:
+        case SK_SIMT_PIPE_CONV_F32: return pipe_valid(sh, v);
         case SK_TC_GEMM_BF16:
         case SK_TC_IGEMM_CONV_BF16: return tc_valid(sh, v);
         case SK_SIMT_DWCONV_F32:

@@ -40,9 +40,9 @@ def test_struct_sizes_match_c_layout():
 
 
 def test_catalogue():
-    assert sketches("dense", "f32") == [0]
-    assert sketches("batch_matmul", "f32") == [0]
-    assert sketches("conv2d", "f32") == [1]
+    assert sketches("dense", "f32") == [0, 7]
+    assert sketches("batch_matmul", "f32") == [0, 7]
+    assert sketches("conv2d", "f32") == [1, 8]
     assert sketches("dense", "bf16") == [2]
     assert sketch_name(0) == "simt_gemm_f32"
     assert knob_names(0) == ["BM", "BN", "BK", "TT", "UNROLL", "VEC", "STAGES", "SPLIT_K"]
@@ -50,6 +50,8 @@ def test_catalogue():
     assert sp[0] == [16, 32, 64, 128] and sp[7] == [1, 2, 4, 8, 16]
     assert knob_names(2) == ["BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER"]
     assert knob_names(3) == ["BM", "BN", "BK", "STAGES", "SPLIT_K", "TILE_Q", "SCHED", "RASTER"]
+    assert sketch_name(8) == "simt_pipe_conv_f32"
+    assert knob_names(8) == ["BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K"]
     assert sketch_name(99) is None
 
 

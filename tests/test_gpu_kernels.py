@@ -46,15 +46,16 @@ def run_points(t, pts, x, w, y):
     return outs
 
 
+@pytest.mark.parametrize("sk", [0, 7])  # simt_gemm_f32, simt_pipe_gemm_f32
 @pytest.mark.parametrize("shape", [(1, 75, 53, 37), (1, 64, 96, 36), (3, 33, 17, 130), (1, 128, 128, 64)])
-def test_simt_gemm_all_configs_vs_oracle(shape):
+def test_simt_gemm_all_configs_vs_oracle(shape, sk):
     b, m, n, k = shape
     op = "dense" if b == 1 else "batch_matmul"
     x, w, yo, ao = gemm_case(b, m, n, k, "uniform", sum(shape))
     xd, wd = to_dev(x, w)
     y = torch.empty(b, m, n, device=dev())
-    t = Tuner(op, {"b": b, "m": m, "n": n, "k": k}, spaces=[(0, sketch_space(0))], x=xd, w=wd, y=y)
-    pts = [p for p in all_points(0) if t.valid(p)]
+    t = Tuner(op, {"b": b, "m": m, "n": n, "k": k}, spaces=[(sk, sketch_space(sk))], x=xd, w=wd, y=y)
+    pts = [p for p in all_points(sk) if t.valid(p)]
     rng = random.Random(0)
     sel = pts if len(pts) <= 700 else rng.sample(pts, 700)
     bad = []
@@ -66,13 +67,14 @@ def test_simt_gemm_all_configs_vs_oracle(shape):
     assert len(sel) > 100
 
 
-def test_simt_gemm_exact_integer_inputs():
+@pytest.mark.parametrize("sk", [0, 7])
+def test_simt_gemm_exact_integer_inputs(sk):
     b, m, n, k = 1, 70, 45, 92
     x, w, yo, _ = gemm_case(b, m, n, k, "int", 5)
     xd, wd = to_dev(x, w)
     y = torch.empty(b, m, n, device=dev())
-    t = Tuner("dense", {"m": m, "n": n, "k": k}, spaces=[(0, sketch_space(0))], x=xd, w=wd, y=y)
-    pts = [p for p in all_points(0) if t.valid(p)]
+    t = Tuner("dense", {"m": m, "n": n, "k": k}, spaces=[(sk, sketch_space(sk))], x=xd, w=wd, y=y)
+    pts = [p for p in all_points(sk) if t.valid(p)]
     for p, yv in run_points(t, random.Random(1).sample(pts, 200), xd, wd, y):
         np.testing.assert_array_equal(yv.reshape(yo.shape), yo.astype(np.float32), err_msg=str(t.values(p)))
 
@@ -87,16 +89,18 @@ CONV_CASES = [
 ]
 
 
+@pytest.mark.parametrize("sk", [1, 8])  # simt_igemm_conv_f32, simt_pipe_conv_f32
 @pytest.mark.parametrize("case", CONV_CASES)
-def test_simt_igemm_conv_vs_oracle(case):
+def test_simt_igemm_conv_vs_oracle(case, sk):
     n, h, wd_, c, k, r, s, st, pd, dl = case
     x, w = tensors([(n, h, wd_, c), (k, r, s, c)], sum(case[:7]))
     yo, ao = oc.conv2d(x, w, st, pd, dl)
     xd, wdd = to_dev(x, w)
     y = torch.empty(yo.shape, device=dev())
     shape = {"N": n, "H": h, "W": wd_, "C": c, "K": k, "R": r, "S": s, "stride": st, "pad": pd, "dil": dl}
-    t = Tuner("conv2d", shape, spaces=[(1, sketch_space(1))], x=xd, w=wdd, y=y)
-    pts = [p for p in all_points(1) if t.valid(p)]
+    t = Tuner("conv2d", shape, spaces=[(sk, sketch_space(sk))], x=xd, w=wdd, y=y)
+    pts = [p for p in all_points(sk) if t.valid(p)]
+    assert len(pts) > 50
     bad = []
     for p, yv in run_points(t, random.Random(2).sample(pts, min(300, len(pts))), xd, wdd, y):
         e = on.max_rel_err(yv, yo, ao)
