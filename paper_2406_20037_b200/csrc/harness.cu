@@ -65,12 +65,16 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
         case SK_SIMT_GEMM_F32:
         case SK_SIMT_IGEMM_CONV_F32:
         case SK_SIMT_IGEMM_CONV_BF16:
-        case SK_SIMT_PIPE_GEMM_F32:  // BM, BN, BK, TT, KW | VEC, STAGES, SPLIT_K
-        case SK_SIMT_PIPE_CONV_F32:
             rk.vec = v[5];
             rk.stages = v[6];
             rk.split = v[7];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[4]));
+        case SK_SIMT_PIPE_GEMM_F32:  // BM, BN, BK, TT, KW, VEC (compiled) | STAGES, SPLIT_K
+        case SK_SIMT_PIPE_CONV_F32:
+            rk.vec = v[5];
+            rk.stages = v[6];
+            rk.split = v[7];
+            return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[4] | (v[5] << 4)));
         case SK_TC_GEMM_BF16:  // BM, BN, BK, STAGES, SPLIT_K, SCHED, RASTER
             rk.split = v[4];
             rk.sched = v[5];

@@ -73,7 +73,7 @@ __device__ __forceinline__ float2 ffma2_ew(float2 a, float2 b, float2 c) {
     return r;
 }
 
-template <int BM, int BN, int BK, int TT, int KW, bool CONV>
+template <int BM, int BN, int BK, int TT, int KW, int VW, bool CONV>
 __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(const PipeParams p) {
     constexpr int TX = BN / TT, TY = BM / TT, GT = TX * TY, NT = GT * KW, LDK = BK + 4, BKG = BK / KW;
     extern __shared__ __align__(16) float smem[];
@@ -93,10 +93,7 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
     const int kt_end = min(p.ktiles, kt_begin + p.kt_per_split);
     if (kt_begin >= kt_end) return;
     const int nk = kt_end - kt_begin;
-    const int vw = p.vw;
-    // chunks per tile row = BK / vw (a power of two): slot -> (row, k) by shifts
-    constexpr int LG_BK = BK == 8 ? 3 : BK == 16 ? 4 : BK == 32 ? 5 : 6;
-    const int lgc = vw == 4 ? LG_BK - 2 : LG_BK, cmask = (1 << lgc) - 1, lgv = vw == 4 ? 2 : 0;
+    constexpr int CPR = BK / VW;  // cp.async chunks per tile row
     const int kbeg = kt_begin * BK;
 
     const float* __restrict__ A = p.A + (CONV ? 0 : bz * p.sA);
@@ -104,15 +101,15 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
     float* __restrict__ C = p.C + bz * p.sC;
 
     // per-slot fixed state: a slot is (row, k chunk) of the tile, the same for every k-tile
-    const int chunksA = BM << lgc, chunksB = BN << lgc;
-    // slots per thread at VEC = 1 (the most), capped by the validity rule
-    constexpr int SA = (BM * BK + NT - 1) / NT < kPipeMaxSlots ? (BM * BK + NT - 1) / NT : kPipeMaxSlots;
-    constexpr int SB = (BN * BK + NT - 1) / NT < kPipeMaxSlots ? (BN * BK + NT - 1) / NT : kPipeMaxSlots;
+    constexpr int chunksA = BM * CPR, chunksB = BN * CPR;
+    constexpr int SA = (chunksA + NT - 1) / NT, SB = (chunksB + NT - 1) / NT;  // slots per thread
+    static_assert(SA <= kPipeMaxSlots && SB <= kPipeMaxSlots, "slot budget (static validity rule)");
+    // A slots: image / row base, h0, w0 (conv) or row offset (dense; h0 = 0 marks a valid row)
     int abase[SA], ah0[SA], aw0[SA];
 #pragma unroll
     for (int i = 0; i < SA; ++i) {
         const int e = tid + i * NT;
-        const int row = e >> lgc;
+        const int row = e / CPR;
         int base = 0, h0 = -(1 << 29), w0 = 0;
         if (e < chunksA && m0 + row < p.M) {
             const int m = m0 + row;
@@ -129,9 +126,9 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
         abase[i] = base; ah0[i] = h0; aw0[i] = w0;
     }
     if constexpr (CONV) {  // koff / tap offsets of every reduction chunk in this CTA's k range
-        const int nent = (nk * BK) >> lgv;
+        const int nent = (nk * BK) / VW;
         for (int j = tid; j < nent; j += NT) {
-            const int kk = kbeg + j * vw;
+            const int kk = kbeg + j * VW;
             int2 t = make_int2(0, 0x7FFF7FFF);  // out of range: fails the image bounds check
             if (kk < p.K) {
                 const int rs = kk / p.Cin, c = kk - rs * p.Cin, r = rs / p.S, s = rs - r * p.S;
@@ -143,6 +140,14 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
         __syncthreads();
     }
 
+    // B slots: element offset of the slot's first k in this CTA's range (-1: row outside N)
+    int boff[SB];
+#pragma unroll
+    for (int i = 0; i < SB; ++i) {
+        const int e = tid + i * NT, row = e / CPR, kl = (e % CPR) * VW;
+        boff[i] = (e < chunksB && n0 + row < p.N) ? (n0 + row) * p.K + kbeg + kl : -1;
+    }
+
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
     auto load_tile = [&](int stage, int kt) {  // kt relative to kt_begin
         const uint32_t as = ring_s + (uint32_t)(stage * STAGE_FLOATS) * 4u;
@@ -151,13 +156,13 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
 #pragma unroll
         for (int i = 0; i < SA; ++i) {
             const int e = tid + i * NT;
-            if (e < chunksA) {
-                const int row = e >> lgc, kl = (e & cmask) << lgv;
+            if (chunksA % NT == 0 || e < chunksA) {
+                const int row = e / CPR, kl = (e % CPR) * VW;
                 const uint32_t dst = as + (uint32_t)(row * LDK + kl) * 4u;
                 const float* src = A;
                 int ok;
                 if constexpr (CONV) {
-                    const int2 t = ktab[(k0 + kl) >> lgv];
+                    const int2 t = ktab[(k0 + kl) / VW];
                     const int h = ah0[i] + (t.y >> 16), w = aw0[i] + (t.y & 0xFFFF);
                     ok = (unsigned)h < (unsigned)p.H && (unsigned)w < (unsigned)p.W;
                     if (ok) src = A + abase[i] + t.x;
@@ -166,20 +171,19 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
                     ok = ah0[i] == 0 && kk < p.K;
                     if (ok) src = A + abase[i] + kk;
                 }
-                if (vw == 4) cp_async16(dst, src, ok ? 16 : 0);
+                if constexpr (VW == 4) cp_async16(dst, src, ok ? 16 : 0);
                 else cp_async4(dst, src, ok ? 4 : 0);
             }
         }
 #pragma unroll
         for (int i = 0; i < SB; ++i) {
             const int e = tid + i * NT;
-            if (e < chunksB) {
-                const int row = e >> lgc, kl = (e & cmask) << lgv;
+            if (chunksB % NT == 0 || e < chunksB) {
+                const int row = e / CPR, kl = (e % CPR) * VW;
                 const uint32_t dst = bs + (uint32_t)(row * LDK + kl) * 4u;
-                const int kk = kbeg + k0 + kl;
-                const bool ok = n0 + row < p.N && kk < p.K;
-                const float* src = ok ? B + (long long)(n0 + row) * p.K + kk : B;
-                if (vw == 4) cp_async16(dst, src, ok ? 16 : 0);
+                const bool ok = boff[i] >= 0 && kbeg + k0 + kl < p.K;
+                const float* src = ok ? B + boff[i] + k0 : B;
+                if constexpr (VW == 4) cp_async16(dst, src, ok ? 16 : 0);
                 else cp_async4(dst, src, ok ? 4 : 0);
             }
         }
@@ -202,13 +206,18 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
             for (int i = 0; i < TT; ++i) a4[i] = *reinterpret_cast<const float4*>(as + (ty + i * TY) * LDK + k);
 #pragma unroll
             for (int j = 0; j < TT; ++j) b4[j] = *reinterpret_cast<const float4*>(bs + (tx + j * TX) * LDK + k);
+            // two passes (k, k+1) then (k+2, k+3): TT*TT independent FFMA2 between the two
+            // updates of one accumulator, so the FMA latency is covered within a warp
 #pragma unroll
             for (int i = 0; i < TT; ++i)
 #pragma unroll
-                for (int j = 0; j < TT; ++j) {
+                for (int j = 0; j < TT; ++j)
                     acc[i][j] = ffma2_ew(make_float2(a4[i].x, a4[i].y), make_float2(b4[j].x, b4[j].y), acc[i][j]);
+#pragma unroll
+            for (int i = 0; i < TT; ++i)
+#pragma unroll
+                for (int j = 0; j < TT; ++j)
                     acc[i][j] = ffma2_ew(make_float2(a4[i].z, a4[i].w), make_float2(b4[j].z, b4[j].w), acc[i][j]);
-                }
         }
     };
 
@@ -217,13 +226,16 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
         if (s < nk) load_tile(s, s);
         cp_commit();
     }
+    int cs = 0, ls = stages - 1;  // stage consumed / stage refilled this iteration (no modulo)
     for (int it = 0; it < nk; ++it) {
         cp_wait_stages(stages);
         __syncthreads();  // tile `it` visible to all; every thread is done with tile it-1's stage
         const int nxt = it + stages - 1;
-        if (nxt < nk) load_tile(nxt % stages, nxt);
+        if (nxt < nk) load_tile(ls, nxt);
         cp_commit();
-        compute(it % stages);
+        compute(cs);
+        cs = cs + 1 == stages ? 0 : cs + 1;
+        ls = ls + 1 == stages ? 0 : ls + 1;
     }
 
     const bool atomic = p.split > 1;
@@ -281,10 +293,10 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
     }
 }
 
-template <int BM, int BN, int BK, int TT, int KW, bool CONV>
+template <int BM, int BN, int BK, int TT, int KW, int VW, bool CONV>
 cudaError_t pipe_launch(const LaunchCtx& c) {
     constexpr int NT = (BM / TT) * (BN / TT) * KW;
-    auto kern = simt_pipe_kernel<BM, BN, BK, TT, KW, CONV>;
+    auto kern = simt_pipe_kernel<BM, BN, BK, TT, KW, VW, CONV>;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -303,7 +315,7 @@ cudaError_t pipe_launch(const LaunchCtx& c) {
     p.kt_per_split = (p.ktiles + c.split - 1) / c.split;
     p.H = (int)s.h; p.W = (int)s.w; p.Cin = (int)s.c; p.P = (int)s.p; p.Q = (int)s.q; p.S = (int)s.s;
     p.sh = s.sh; p.sw = s.sw; p.ph = s.ph; p.pw = s.pw; p.dh = s.dh; p.dw = s.dw;
-    p.vw = c.vec == 4 ? 4 : 1;
+    p.vw = VW;
     p.stages = c.stages;
     if (c.split > 1) {
         cudaError_t e = cudaMemsetAsync(c.y, 0, (size_t)s.y_elems * sizeof(float), c.stream);
@@ -318,9 +330,12 @@ cudaError_t pipe_launch(const LaunchCtx& c) {
 
 template <int BM, int BN, int BK, int TT, int KW, bool CONV>
 void pipe_register() {
-    if constexpr (pipe_static_ok(BM, BN, BK, TT, KW)) {
-        registry_add(kernel_key(CONV ? SK_SIMT_PIPE_CONV_F32 : SK_SIMT_PIPE_GEMM_F32, BM, BN, BK, TT, KW),
-                     &pipe_launch<BM, BN, BK, TT, KW, CONV>);
+    if constexpr (pipe_static_ok(BM, BN, BK, TT, KW)) {  // VEC is compiled too: key field = KW | VEC << 4
+        constexpr int32_t sk = CONV ? SK_SIMT_PIPE_CONV_F32 : SK_SIMT_PIPE_GEMM_F32;
+        constexpr int NT = (BM / TT) * (BN / TT) * KW;
+        registry_add(kernel_key(sk, BM, BN, BK, TT, KW | (4 << 4)), &pipe_launch<BM, BN, BK, TT, KW, 4, CONV>);
+        if constexpr ((BM * BK + NT - 1) / NT <= kPipeMaxSlots && (BN * BK + NT - 1) / NT <= kPipeMaxSlots)
+            registry_add(kernel_key(sk, BM, BN, BK, TT, KW | (1 << 4)), &pipe_launch<BM, BN, BK, TT, KW, 1, CONV>);
     }
 }
 

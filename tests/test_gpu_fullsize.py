@@ -8,7 +8,7 @@ import torch
 
 from oracle import contractions as oc
 from oracle import numerics as on
-from paper_2406_20037_b200 import Tuner
+from paper_2406_20037_b200 import Tuner, sketch_space
 from synth import BERT, CONFIG1, RESNET18, RESNET50, VGG16, layer_tensors
 from synth.workloads import out_hw
 
@@ -30,7 +30,7 @@ def out_shape(L):
     return (L.get("b", 1), L["m"], L["n"])
 
 
-def tune_and_check(L, dtype, n_sample, samples=3000, seed=0):
+def tune_and_check(L, dtype, n_sample, samples=3000, seed=0, sketch=None):
     x, w = layer_tensors(L, 0x5EED)
     if dtype == "bf16":
         x, w = on.round_bf16(x), on.round_bf16(w)
@@ -38,7 +38,8 @@ def tune_and_check(L, dtype, n_sample, samples=3000, seed=0):
     xd = torch.from_numpy(x).to(DEV).to(tdt)
     wd = torch.from_numpy(w).to(DEV).to(tdt)
     y = torch.empty(out_shape(L), device=DEV)
-    t = Tuner(L["op"], shape_of(L), dtype=dtype, x=xd, w=wd, y=y, seed=seed, early_cut=4.0)
+    spaces = None if sketch is None else [(sketch, sketch_space(sketch))]
+    t = Tuner(L["op"], shape_of(L), dtype=dtype, x=xd, w=wd, y=y, seed=seed, early_cut=4.0, spaces=spaces)
     smp = t.sample(n_sample)
     assert smp and all(s.status == "ok" for s in smp), [s for s in smp if s.status != "ok"][:3]
     rep = t.droplet(t.best().point, 100)
@@ -64,6 +65,12 @@ def tune_and_check(L, dtype, n_sample, samples=3000, seed=0):
 @pytest.mark.parametrize("L", [RESNET18[0], RESNET18[1], RESNET50[20], CONFIG1], ids=lambda L: L["name"])
 def test_fullsize_fp32(L):
     print(tune_and_check(L, "f32", 300))
+
+
+@pytest.mark.parametrize("L", [RESNET18[0], RESNET18[10], RESNET50[3], CONFIG1], ids=lambda L: L["name"])
+def test_fullsize_fp32_pipe_sketch(L):
+    # the cp.async multistage sketch alone (simt_pipe_conv_f32 / simt_pipe_gemm_f32)
+    print(tune_and_check(L, "f32", 300, sketch=8 if L["op"] == "conv2d" else 7))
 
 
 @pytest.mark.parametrize("L", [VGG16[1], VGG16[7], BERT[2], BERT[4]], ids=lambda L: L["name"])

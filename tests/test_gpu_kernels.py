@@ -109,6 +109,22 @@ def test_simt_igemm_conv_vs_oracle(case, sk):
     assert not bad, bad[:5]
 
 
+@pytest.mark.parametrize("sk", [1, 8])
+def test_simt_conv_exact_integer_inputs(sk):
+    # integer inputs in {-2..2}: every partial sum is exact in fp32, so any summation order
+    # (split-K atomics, sliced-K groups, k-parity halves) must reproduce the oracle bit for bit
+    n, h, wd_, c, k, r, s = 2, 11, 9, 12, 20, 3, 3
+    x, w = tensors([(n, h, wd_, c), (k, r, s, c)], 9, "int")
+    yo, _ = oc.conv2d(x, w, (2, 1), (1, 1))
+    xd, wdd = to_dev(x, w)
+    y = torch.empty(yo.shape, device=dev())
+    shape = {"N": n, "H": h, "W": wd_, "C": c, "K": k, "R": r, "S": s, "stride": (2, 1), "pad": (1, 1)}
+    t = Tuner("conv2d", shape, spaces=[(sk, sketch_space(sk))], x=xd, w=wdd, y=y)
+    pts = [p for p in all_points(sk) if t.valid(p)]
+    for p, yv in run_points(t, random.Random(4).sample(pts, 200), xd, wdd, y):
+        np.testing.assert_array_equal(yv, yo.astype(np.float32), err_msg=str(t.values(p)))
+
+
 def test_naive_reference_vs_oracle():
     x, w = tensors([(2, 10, 9, 5), (7, 3, 3, 5)], 3)
     yo, ao = oc.conv2d(x, w, (2, 1), (1, 1))
