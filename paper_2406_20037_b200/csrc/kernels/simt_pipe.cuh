@@ -196,28 +196,41 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
         for (int j = 0; j < TT; ++j) acc[i][j] = make_float2(0.f, 0.f);
 
     auto compute = [&](int stage) {
-        const float* as = ring + stage * STAGE_FLOATS;
-        const float* bs = as + BM * LDK;
+        const float* as = ring + stage * STAGE_FLOATS + ty * LDK + g * BKG;
+        const float* bs = ring + stage * STAGE_FLOATS + BM * LDK + tx * LDK + g * BKG;
+        constexpr int NKQ = BKG / 4;
+        // register double buffer: the fragments of step kq+1 are loaded before the FFMA2s of
+        // step kq, so shared-memory latency overlaps the math within one warp
+        float4 a4[2][TT], b4[2][TT];
 #pragma unroll
-        for (int kq = 0; kq < BKG / 4; ++kq) {
-            const int k = g * BKG + kq * 4;
-            float4 a4[TT], b4[TT];
+        for (int i = 0; i < TT; ++i) a4[0][i] = *reinterpret_cast<const float4*>(as + i * TY * LDK);
 #pragma unroll
-            for (int i = 0; i < TT; ++i) a4[i] = *reinterpret_cast<const float4*>(as + (ty + i * TY) * LDK + k);
+        for (int j = 0; j < TT; ++j) b4[0][j] = *reinterpret_cast<const float4*>(bs + j * TX * LDK);
 #pragma unroll
-            for (int j = 0; j < TT; ++j) b4[j] = *reinterpret_cast<const float4*>(bs + (tx + j * TX) * LDK + k);
+        for (int kq = 0; kq < NKQ; ++kq) {
+            const int cur = kq & 1;
+            if (kq + 1 < NKQ) {
+#pragma unroll
+                for (int i = 0; i < TT; ++i)
+                    a4[cur ^ 1][i] = *reinterpret_cast<const float4*>(as + i * TY * LDK + (kq + 1) * 4);
+#pragma unroll
+                for (int j = 0; j < TT; ++j)
+                    b4[cur ^ 1][j] = *reinterpret_cast<const float4*>(bs + j * TX * LDK + (kq + 1) * 4);
+            }
             // two passes (k, k+1) then (k+2, k+3): TT*TT independent FFMA2 between the two
-            // updates of one accumulator, so the FMA latency is covered within a warp
+            // updates of one accumulator
 #pragma unroll
             for (int i = 0; i < TT; ++i)
 #pragma unroll
                 for (int j = 0; j < TT; ++j)
-                    acc[i][j] = ffma2_ew(make_float2(a4[i].x, a4[i].y), make_float2(b4[j].x, b4[j].y), acc[i][j]);
+                    acc[i][j] = ffma2_ew(make_float2(a4[cur][i].x, a4[cur][i].y),
+                                         make_float2(b4[cur][j].x, b4[cur][j].y), acc[i][j]);
 #pragma unroll
             for (int i = 0; i < TT; ++i)
 #pragma unroll
                 for (int j = 0; j < TT; ++j)
-                    acc[i][j] = ffma2_ew(make_float2(a4[i].z, a4[i].w), make_float2(b4[j].z, b4[j].w), acc[i][j]);
+                    acc[i][j] = ffma2_ew(make_float2(a4[cur][i].z, a4[cur][i].w),
+                                         make_float2(b4[cur][j].z, b4[cur][j].w), acc[i][j]);
         }
     };
 

@@ -9,7 +9,7 @@ import torch
 
 from oracle import contractions as oc
 from oracle import numerics as on
-from paper_2406_20037_b200 import Tuner, global_launch_count, sketch_space
+from paper_2406_20037_b200 import Tuner, global_launch_count, sketch_space, sketches
 from synth import tensors
 
 pytestmark = pytest.mark.gpu
@@ -159,15 +159,19 @@ def test_harness_sample_droplet_and_replay():
     log = {(s.point[0], s.point[1]): s.cost_ns for s in t.history()}
     # record/replay: the oracle's Droplet over the logged costs
     # reproduces the GPU trajectory and never asks for an unlogged point
-    sp = Space([sketch_space(0)])
-    to_o = lambda p: (0, p[1])
+    # the oracle's points are (position in the space list, index vector); the library's
+    # are (sketch id, index vector): the default dense f32 spaces are every f32 dense sketch
+    sks = sketches("dense", "f32")
+    sp = Space([sketch_space(s) for s in sks])
+    to_o = lambda p: (sks.index(p[0]), tuple(p[1]))
+    to_l = lambda p: (sks[p[0]], tuple(p[1]))
 
     def cost(p):
-        return log[(0, p[1])]
-    ot = OracleTuner(sp, cost, lambda p: (0, p[1]) in log)
+        return log[to_l(p)]
+    ot = OracleTuner(sp, cost, lambda p: to_l(p) in log)
     ot.measure([to_o(p) for p in pre])
     orep = ot.droplet(to_o(b.point), 100, "grow")
-    assert [p[1] for p in orep["traj"]] == [p[1] for p in rep["traj"]]
+    assert [to_l(p) for p in orep["traj"]] == [(p[0], tuple(p[1])) for p in rep["traj"]]
     assert orep["trials_used"] == rep["trials_used"] and orep["converged"] == rep["converged"]
     # the chosen schedule really computes the layer
     t.run(rep["best"], xd, wd, y)

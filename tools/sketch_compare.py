@@ -19,25 +19,27 @@ def main():
     ap.add_argument("--sketches", default="1,8")
     ap.add_argument("--n", type=int, default=2000)
     ap.add_argument("--top", type=int, default=3)
+    ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--seed", type=int, default=1)
     a = ap.parse_args()
     import torch
 
     from paper_2406_20037_b200 import Tuner, sketch_space
-    from synth import CONFIG1, RESNET18, RESNET50, layer_flops, layer_tensors
+    from synth import ALEXNET, BERT, CONFIG1, RESNET18, RESNET50, VGG16, layer_flops, layer_tensors
     from synth.workloads import out_hw
 
-    allL = {L["name"]: L for L in RESNET18 + RESNET50 + [CONFIG1]}
-    if a.layers == "r18":
-        names = [L["name"] for L in RESNET18]
-    elif a.layers == "r50":
-        names = [L["name"] for L in RESNET50]
+    allL = {L["name"]: L for L in RESNET18 + RESNET50 + VGG16 + ALEXNET + BERT + [CONFIG1]}
+    groups = {"r18": RESNET18, "r50": RESNET50, "vgg": VGG16, "alex": ALEXNET, "bert": BERT}
+    tdt = torch.float32 if a.dtype == "f32" else torch.bfloat16
+    if a.layers in groups:
+        names = [L["name"] for L in groups[a.layers]]
     else:
         names = a.layers.split(",")
     dev = torch.device("cuda:0")
     for name in names:
         L = allL[name]
         x, w = layer_tensors(L, 1)
-        xd, wd = torch.from_numpy(x).to(dev), torch.from_numpy(w).to(dev)
+        xd, wd = torch.from_numpy(x).to(dev).to(tdt), torch.from_numpy(w).to(dev).to(tdt)
         if L["op"] == "conv2d":
             P, Q = out_hw(L)
             y = torch.empty((L["N"], P, Q, L["K"]), device=dev)
@@ -46,8 +48,12 @@ def main():
             y = torch.empty((L.get("b", 1), L["m"], L["n"]), device=dev)
             shape = {k: L[k] for k in ("b", "m", "n", "k") if k in L}
         for sk in [int(s) for s in a.sketches.split(",")]:
-            t = Tuner(L["op"], shape, spaces=[(sk, sketch_space(sk))], x=xd, w=wd, y=y, seed=1)
+            t = Tuner(L["op"], shape, dtype=a.dtype, spaces=[(sk, sketch_space(sk))], x=xd, w=wd, y=y, seed=a.seed)
             smp = t.sample(a.n)
+            if not smp:
+                print(json.dumps({"layer": name, "sketch": sk, "n": 0}), flush=True)
+                t.close()
+                continue
             ok = sorted([s for s in smp if s.status == "ok"], key=lambda s: s.cost_ns)
             wrong = sum(s.status == "wrong" for s in smp)
             top = [(t.values(s.point), round(s.cost_ns)) for s in ok[: a.top]]
