@@ -40,6 +40,14 @@ void set_capturing(bool on);
 
 static constexpr int kMaxGraphNodes = 8;     // launches per captured graph
 static constexpr double kLightFactor = 1.5;
+// precise tier (R-M4): with early_cut on, candidates whose repeat-timed cost is within
+// kPreciseFactor of the best cost known (incumbent or this batch) are re-timed over
+// kPreciseWindows windows of >= kPreciseWindowNs each; their cost is the mean of those.
+// Event-timed windows on this GPU are quantised to ~1-2 us (tools/launch_quantum_probe.py),
+// i.e. ~5-10 % of a 20 us repeat: the long windows bring that to <~1 % where decisions are made.
+static constexpr double kPreciseFactor = 1.08;
+static constexpr int kPreciseWindows = 2;
+static constexpr double kPreciseWindowNs = 200000.0;
 static constexpr size_t kExecCache = 16;     // cached timing-graph executables per measurer  // early-cut mode: > 1.5x the best -> 3 repeats
 
 static tuner_status cuda_fail(cudaError_t e, const char* what) {
@@ -162,6 +170,10 @@ struct GpuMeasurer : Measurer {
         return cudaSuccess;
     }
     std::vector<cudaGraphExec_t> transient;
+    // like-for-like references for the tiers: the best verify-run time and the best
+    // repeat-timed (coarse) cost this measurer has seen.  The incumbent's cost may be a
+    // precise one (R-M4), which is systematically below both, so it is not compared with them.
+    double best_tver = INFINITY, best_coarse = INFINITY;
 
     ~GpuMeasurer() override {
         int cur = 0;
@@ -212,7 +224,8 @@ struct GpuMeasurer : Measurer {
         if (n == 0) return TUNER_OK;
         CU(cudaSetDevice(dev));
         const int R = t->opts.repeats, W = t->opts.warmup;
-        tuner_status s = ensure_events(dev, n * (size_t)(R + 3));
+        const size_t EB = (size_t)R + 1 + kPreciseWindows;  // timing events per candidate
+        tuner_status s = ensure_events(dev, 2 * n + n * EB);
         if (s != TUNER_OK) return s;
         auto& ev = event_pool(dev);
         if (err_cap < n) {
@@ -279,10 +292,12 @@ struct GpuMeasurer : Measurer {
         // and time clearly non-competitive ones (> 1.5x) with 3 repeats instead of R
         std::vector<char> cut(n, 0);
         std::vector<int> reps(n, R), warm(n, W);
+        (void)incumbent;
         if (t->opts.early_cut > 0.0) {
-            double ref_ns = incumbent;
+            double ref_ns = best_tver;
             for (size_t j = 0; j < n; ++j)
                 if (out[j].status == TUNER_S_OK) ref_ns = std::min(ref_ns, tver[j]);
+            best_tver = ref_ns;
             for (size_t j = 0; j < n; ++j) {
                 if (out[j].status != TUNER_S_OK) continue;
                 if (tver[j] > t->opts.early_cut * ref_ns) cut[j] = 1;
@@ -297,24 +312,13 @@ struct GpuMeasurer : Measurer {
         std::vector<cudaGraphExec_t> execs(n, nullptr);
         std::vector<int> number(n, 1);
         const size_t tb = 2 * n;  // timing events start here
-        for (size_t j = 0; j < n; ++j) {
-            if (out[j].status != TUNER_S_OK || cut[j]) continue;
-            set_knobs(j);
-            int num = t->opts.number;
-            if (num <= 0) {
-                double want = 20000.0 / std::max(tver[j], 1.0);
-                num = (int)std::min(100.0, std::max(1.0, std::ceil(want)));
-            }
-            // a graph of G <= 8 launches replayed L times per repeat: few nodes to capture
-            // and instantiate on the host, and back-to-back launches on the device
+        // nwin back-to-back windows of `num` launches each, bracketed by events ev[b..b+nwin]:
+        // a graph of G <= 8 launches replayed L times per window (few nodes to capture and
+        // instantiate on the host, back-to-back launches on the device); returns G * L
+        auto time_windows = [&](size_t j, int num, int nwin, size_t b, int& used) -> tuner_status {
             const int G = std::min(num, kMaxGraphNodes);
-            const int Lr = (num + G - 1) / G;
-            num = G * Lr;
-            number[j] = num;
-            for (int i = 0; i < warm[j]; ++i) {
-                cudaError_t e = fn[j](ctx);
-                if (e != cudaSuccess) return cuda_fail(e, "warm-up launch");
-            }
+            const int L = (num + G - 1) / G;
+            used = G * L;
             LaunchCtx cc = ctx;
             cc.stream = cap;
             set_capturing(true);
@@ -328,13 +332,28 @@ struct GpuMeasurer : Measurer {
             e = exec_for(g, execs[j]);
             cudaGraphDestroy(g);
             if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-            const size_t b = tb + j * (size_t)(R + 1);
             CU(cudaEventRecord(ev[b], st));
-            for (int r = 0; r < reps[j]; ++r) {
-                for (int l = 0; l < Lr; ++l) CU(cudaGraphLaunch(execs[j], st));
-                count_launches(num);
+            for (int r = 0; r < nwin; ++r) {
+                for (int l = 0; l < L; ++l) CU(cudaGraphLaunch(execs[j], st));
+                count_launches(used);
                 CU(cudaEventRecord(ev[b + r + 1], st));
             }
+            return TUNER_OK;
+        };
+        for (size_t j = 0; j < n; ++j) {
+            if (out[j].status != TUNER_S_OK || cut[j]) continue;
+            set_knobs(j);
+            int num = t->opts.number;
+            if (num <= 0) {
+                double want = 20000.0 / std::max(tver[j], 1.0);
+                num = (int)std::min(100.0, std::max(1.0, std::ceil(want)));
+            }
+            for (int i = 0; i < warm[j]; ++i) {
+                cudaError_t e = fn[j](ctx);
+                if (e != cudaSuccess) return cuda_fail(e, "warm-up launch");
+            }
+            tuner_status ts = time_windows(j, num, reps[j], tb + j * EB, number[j]);
+            if (ts != TUNER_OK) return ts;
         }
         cudaError_t se = cudaStreamSynchronize(st);
         for (auto ge : transient) cudaGraphExecDestroy(ge);
@@ -352,7 +371,7 @@ struct GpuMeasurer : Measurer {
                 out[j].samp[0] = (float)tver[j];
                 continue;
             }
-            const size_t b = tb + j * (size_t)(R + 1);
+            const size_t b = tb + j * EB;
             const int Rj = reps[j];
             for (int r = 0; r < Rj; ++r) {
                 float ms = 0.f;
@@ -371,6 +390,44 @@ struct GpuMeasurer : Measurer {
                 out[j].cost_ns = sum / (Rj - 2);
             } else {
                 out[j].cost_ns = (Rj % 2) ? per[Rj / 2] : 0.5 * (per[Rj / 2 - 1] + per[Rj / 2]);
+            }
+        }
+
+        // ---- phase 3 (R-M4): long windows for the candidates near the best known cost
+        if (t->opts.early_cut > 0.0 && t->opts.number <= 0) {
+            double best = best_coarse;
+            for (size_t j = 0; j < n; ++j)
+                if (out[j].status == TUNER_S_OK && !cut[j]) best = std::min(best, out[j].cost_ns);
+            best_coarse = best;
+            std::vector<char> precise(n, 0);
+            std::vector<int> nlong(n, 0);
+            bool any = false;
+            for (size_t j = 0; j < n; ++j) {
+                if (out[j].status != TUNER_S_OK || cut[j] || !(out[j].cost_ns <= kPreciseFactor * best)) continue;
+                precise[j] = 1;
+                any = true;
+                set_knobs(j);
+                const double want = kPreciseWindowNs / std::max(out[j].cost_ns, 1.0);
+                const int num = (int)std::min(4000.0, std::max(1.0, std::ceil(want)));
+                tuner_status ts = time_windows(j, num, kPreciseWindows, tb + j * EB + (size_t)reps[j], nlong[j]);
+                if (ts != TUNER_OK) return ts;
+            }
+            if (any) {
+                cudaError_t se3 = cudaStreamSynchronize(st);
+                for (auto ge : transient) cudaGraphExecDestroy(ge);
+                transient.clear();
+                if (se3 != cudaSuccess) return cuda_fail(se3, "cudaStreamSynchronize (precise timing)");
+                for (size_t j = 0; j < n; ++j) {
+                    if (!precise[j]) continue;
+                    const size_t b = tb + j * EB + (size_t)reps[j];
+                    double sum = 0.0;
+                    for (int r = 0; r < kPreciseWindows; ++r) {
+                        float ms = 0.f;
+                        CU(cudaEventElapsedTime(&ms, ev[b + r], ev[b + r + 1]));
+                        sum += (double)ms * 1e6 / nlong[j];
+                    }
+                    out[j].cost_ns = sum / kPreciseWindows;
+                }
             }
         }
         return TUNER_OK;

@@ -11,7 +11,7 @@ namespace db200 {
 DECL_SIMT(0, 16) DECL_SIMT(0, 32) DECL_SIMT(0, 64) DECL_SIMT(0, 128)
 DECL_SIMT(1, 16) DECL_SIMT(1, 32) DECL_SIMT(1, 64) DECL_SIMT(1, 128)
 #define DECL_PIPE(c, bm) void register_simt_pipe_c##c##_bm##bm();
-DECL_PIPE(0, 32) DECL_PIPE(0, 64) DECL_PIPE(0, 128) DECL_PIPE(1, 32) DECL_PIPE(1, 64) DECL_PIPE(1, 128)
+DECL_PIPE(0, 16) DECL_PIPE(0, 32) DECL_PIPE(0, 64) DECL_PIPE(0, 128) DECL_PIPE(1, 16) DECL_PIPE(1, 32) DECL_PIPE(1, 64) DECL_PIPE(1, 128)
 void register_tc_gemm();
 void register_simt_bf16_conv();
 void register_dwconv();
@@ -25,8 +25,8 @@ static std::once_flag g_once;
 static void init_all() {
     register_simt_c0_bm16(); register_simt_c0_bm32(); register_simt_c0_bm64(); register_simt_c0_bm128();
     register_simt_c1_bm16(); register_simt_c1_bm32(); register_simt_c1_bm64(); register_simt_c1_bm128();
-    register_simt_pipe_c0_bm32(); register_simt_pipe_c0_bm64(); register_simt_pipe_c0_bm128();
-    register_simt_pipe_c1_bm32(); register_simt_pipe_c1_bm64(); register_simt_pipe_c1_bm128();
+    register_simt_pipe_c0_bm16(); register_simt_pipe_c0_bm32(); register_simt_pipe_c0_bm64(); register_simt_pipe_c0_bm128();
+    register_simt_pipe_c1_bm16(); register_simt_pipe_c1_bm32(); register_simt_pipe_c1_bm64(); register_simt_pipe_c1_bm128();
     register_tc_gemm();
     register_simt_bf16_conv();
     register_dwconv();

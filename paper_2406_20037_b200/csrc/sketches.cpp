@@ -25,8 +25,9 @@ static std::vector<SketchDesc> build_catalogue() {
     // ring with zero-fill gathers, KW warp groups slicing each staged k-tile (summed through
     // shared memory), k-parity FFMA2 accumulators; VEC = cp.async width, SPLIT_K as above.
     const std::vector<const char*> pipe_names = {"BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K"};
-    const std::vector<std::vector<int32_t>> pipe_vals = {{32, 64, 128}, {32, 64, 128}, {8, 16, 32}, {2, 4},
-                                                         {1, 2, 4},     {1, 4},        {2, 3, 4, 6}, {1, 2, 4, 8, 16}};
+    const std::vector<std::vector<int32_t>> pipe_vals = {{16, 32, 64, 128}, {32, 64, 128}, {8, 16, 32},
+                                                         {2, 4},            {1, 2, 4},     {1, 4},
+                                                         {2, 3, 4, 6},      {1, 2, 4, 8, 16, 32}};
     c.push_back({SK_SIMT_PIPE_GEMM_F32, "simt_pipe_gemm_f32", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL),
                  TUNER_F32, pipe_names, pipe_vals});
     c.push_back({SK_SIMT_PIPE_CONV_F32, "simt_pipe_conv_f32", 1 << TUNER_OP_CONV2D, TUNER_F32, pipe_names,

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--top", type=int, default=3)
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--early-cut", type=float, default=4.0, help="bench setting; > 0 also enables the precise tier")
     a = ap.parse_args()
     import torch
 
@@ -48,7 +49,8 @@ def main():
             y = torch.empty((L.get("b", 1), L["m"], L["n"]), device=dev)
             shape = {k: L[k] for k in ("b", "m", "n", "k") if k in L}
         for sk in [int(s) for s in a.sketches.split(",")]:
-            t = Tuner(L["op"], shape, dtype=a.dtype, spaces=[(sk, sketch_space(sk))], x=xd, w=wd, y=y, seed=a.seed)
+            t = Tuner(L["op"], shape, dtype=a.dtype, spaces=[(sk, sketch_space(sk))], x=xd, w=wd, y=y, seed=a.seed,
+                      early_cut=a.early_cut)
             smp = t.sample(a.n)
             if not smp:
                 print(json.dumps({"layer": name, "sketch": sk, "n": 0}), flush=True)
