@@ -35,4 +35,18 @@ LaunchFn registry_find(uint64_t key);
 void count_launches(int64_t n);
 void set_capturing(bool on);
 
+// Split-K zeroing as a kernel that lets the partial-sum kernel launch early (programmatic
+// dependent launch): the dependent kernel stages and multiplies while Y is being zeroed and
+// waits (griddep_wait) only before its first atomic.  Replaces cudaMemsetAsync + full
+// stream serialisation: the zeroing node's launch and run time leave the critical path.
+cudaError_t zero_for_splitk(float* y, long long n, cudaStream_t st);
+// launch attribute for the dependent kernel (cudaLaunchKernelEx)
+inline void pdl_attr(cudaLaunchAttribute& a) {
+    a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a.val.programmaticStreamSerializationAllowed = 1;
+}
+// wait until the prerequisite grid (the zeroing kernel) has completed and its writes are
+// visible; returns at once for a kernel launched without a programmatic dependency
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace db200

@@ -172,6 +172,25 @@ cudaError_t launch_reference(const ShapeInfo& s, const void* x, const void* w, f
     return cudaGetLastError();
 }
 
+// split-K zeroing: dependents may launch as soon as every CTA of this grid has started
+__global__ void zero_splitk(float4* __restrict__ y4, long long n4, float* __restrict__ tail, int ntail) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride)
+        y4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (blockIdx.x == 0 && (int)threadIdx.x < ntail) tail[threadIdx.x] = 0.f;
+}
+
+cudaError_t zero_for_splitk(float* y, long long n, cudaStream_t st) {
+    const long long n4 = n / 4;  // Y is a cudaMalloc'ed fp32 tensor: 16-byte aligned
+    const int ntail = (int)(n - 4 * n4);
+    long long blocks = (n4 + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    zero_splitk<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<float4*>(y), n4, y + 4 * n4, ntail);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_verify(const float* y, const float* r, const float* a, long long n, unsigned int* out,
                           int num_sms, cudaStream_t st) {
     const int bs = 512;

@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
 
     // epilogue: direct stores (SPLIT_K = 1) or atomic partial-sum reduction
     const bool atomic = p.split > 1;
+    if (atomic) griddep_wait();  // Y zeroed by the prerequisite grid (PDL)
 #pragma unroll
     for (int i = 0; i < TT; ++i) {
         const int m = m0 + tile_row<BM, TT>(ty, i);
@@ -392,12 +393,23 @@ cudaError_t simt_launch(const LaunchCtx& c) {
     p.vec4 = c.vec == 4;
     p.stages = c.stages;
     if (c.split > 1) {
-        cudaError_t e = cudaMemsetAsync(c.y, 0, (size_t)s.y_elems * sizeof(float), c.stream);
+        cudaError_t e = zero_for_splitk((float*)c.y, s.y_elems, c.stream);
         if (e != cudaSuccess) return e;
     }
-    dim3 grid((unsigned)((s.M + BM - 1) / BM), (unsigned)((s.N + BN - 1) / BN), (unsigned)(s.batch * c.split));
-    kern<<<grid, Cfg::NT, Cfg::SMEM, c.stream>>>(p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((s.M + BM - 1) / BM), (unsigned)((s.N + BN - 1) / BN), (unsigned)(s.batch * c.split));
+    cfg.blockDim = dim3(Cfg::NT);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    if (c.split > 1) {  // launch early; the kernel waits for the zeroing before its atomics
+        pdl_attr(attr[0]);
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
     count_launches(1);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

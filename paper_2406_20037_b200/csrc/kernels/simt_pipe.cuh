@@ -81,7 +81,8 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
     float* ring = smem;  // [stages][(BM + BN) * LDK]
     constexpr int STAGE_FLOATS = (BM + BN) * LDK;
     const size_t pipe_floats = (size_t)stages * STAGE_FLOATS;
-    const size_t red_floats = KW > 1 ? (size_t)KW * BM * BN : 0;
+    const bool staged_epi = KW > 1 || p.split > 1;  // epilogue through shared memory
+    const size_t red_floats = staged_epi ? (size_t)KW * BM * BN : 0;
     int2* ktab = reinterpret_cast<int2*>(smem + (pipe_floats > red_floats ? pipe_floats : red_floats));
 
     const int tid = threadIdx.x;
@@ -252,7 +253,8 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
     }
 
     const bool atomic = p.split > 1;
-    if constexpr (KW == 1) {
+    if (atomic) griddep_wait();  // Y zeroed by the prerequisite grid (PDL)
+    if (!staged_epi) {  // KW = 1, no split-K: direct stores from the accumulators
 #pragma unroll
         for (int i = 0; i < TT; ++i) {
             const int m = m0 + ty + i * TY;
@@ -268,7 +270,8 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
                 }
             }
         }
-    } else {  // sliced-K: the KW groups' partial tiles are summed through shared memory
+    } else {  // the KW groups' partial tiles summed through shared memory; 128-bit stores or
+              // (split-K) 128-bit atomics from the staged tile
         cp_wait<0>();
         __syncthreads();
         float* red = smem;  // [KW][BM][BN]
@@ -331,13 +334,24 @@ cudaError_t pipe_launch(const LaunchCtx& c) {
     p.vw = VW;
     p.stages = c.stages;
     if (c.split > 1) {
-        cudaError_t e = cudaMemsetAsync(c.y, 0, (size_t)s.y_elems * sizeof(float), c.stream);
+        cudaError_t e = zero_for_splitk((float*)c.y, s.y_elems, c.stream);
         if (e != cudaSuccess) return e;
     }
-    const size_t smem = pipe_smem_bytes(BM, BN, BK, KW, p.stages, CONV, p.kt_per_split * BK, p.vw);
-    dim3 grid((unsigned)((s.M + BM - 1) / BM), (unsigned)((s.N + BN - 1) / BN), (unsigned)(s.batch * c.split));
-    kern<<<grid, NT, smem, c.stream>>>(p);
+    const size_t smem = pipe_smem_bytes(BM, BN, BK, KW, p.stages, CONV, p.kt_per_split * BK, p.vw, p.split);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((s.M + BM - 1) / BM), (unsigned)((s.N + BN - 1) / BN), (unsigned)(s.batch * c.split));
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    if (c.split > 1) {  // launch early; the kernel waits for the zeroing before its atomics
+        pdl_attr(attr[0]);
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
     count_launches(1);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

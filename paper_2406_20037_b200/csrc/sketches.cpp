@@ -158,7 +158,7 @@ static bool pipe_valid(const ShapeInfo& sh, const int32_t* v) {
     const int64_t ktiles = (sh.K + bk - 1) / bk;
     if (split > ktiles) return false;
     const int64_t kspan = ((ktiles + split - 1) / split) * bk;
-    if (pipe_smem_bytes(bm, bn, bk, kw, stages, conv, (int)kspan, vec) > 227 * 1024) return false;
+    if (pipe_smem_bytes(bm, bn, bk, kw, stages, conv, (int)kspan, vec, split) > 227 * 1024) return false;
     const int64_t ntiles = (sh.N + bn - 1) / bn;
     if (ntiles > 65535 || (int64_t)split * sh.batch > 65535) return false;
     if (conv && (sh.r - 1) * sh.dh >= 32767) return false;  // tap offsets packed in 16 bits
