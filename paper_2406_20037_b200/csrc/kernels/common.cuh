@@ -40,10 +40,12 @@ void set_capturing(bool on);
 // waits (griddep_wait) only before its first atomic.  Replaces cudaMemsetAsync + full
 // stream serialisation: the zeroing node's launch and run time leave the critical path.
 cudaError_t zero_for_splitk(float* y, long long n, cudaStream_t st);
-// launch attribute for the dependent kernel (cudaLaunchKernelEx)
+// launch attribute for the dependent kernel (cudaLaunchKernelEx); DB200_NO_PDL=1 turns the
+// early launch off (plain stream serialisation) for A/B timing
+bool pdl_enabled();
 inline void pdl_attr(cudaLaunchAttribute& a) {
     a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    a.val.programmaticStreamSerializationAllowed = 1;
+    a.val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
 }
 // wait until the prerequisite grid (the zeroing kernel) has completed and its writes are
 // visible; returns at once for a kernel launched without a programmatic dependency

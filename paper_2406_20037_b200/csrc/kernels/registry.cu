@@ -1,5 +1,6 @@
 // registry.cu — (sketch, compile-time knobs) -> launcher table.
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -52,5 +53,13 @@ void count_launches(int64_t n) {
     if (!g_capturing) g_launches.fetch_add(n, std::memory_order_relaxed);
 }
 std::atomic<int64_t>* g_launch_counter_ptr() { return &g_launches; }
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DB200_NO_PDL");
+        return !(e && e[0] && e[0] != '0');
+    }();
+    return on;
+}
 
 }  // namespace db200

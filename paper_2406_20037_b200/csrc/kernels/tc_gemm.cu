@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(192, 1)
             }
         }
     } else {  // ---- epilogue: TMEM -> registers -> global
+        if (p.split > 1) griddep_wait();  // split-K: Y zeroed by the prerequisite grid (PDL)
         const int q = warp & 3;
         const int trow = q * 32 + lane;  // row of the 128-row sub-tile held by this thread
         const bool vec_ok = (p.N % 4) == 0;  // TMA needs 16-byte global strides
@@ -659,7 +660,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     p.raster = c.raster;
     p.total_iters = tiles * p.kblocks;
     if (c.split > 1) {
-        cudaError_t e = cudaMemsetAsync(c.y, 0, (size_t)s.y_elems * sizeof(float), c.stream);
+        cudaError_t e = zero_for_splitk((float*)c.y, s.y_elems, c.stream);
         if (e != cudaSuccess) return e;
     }
     // persistent grid: CTA groups = SMs / CG x resident slots (shared memory and TMEM limited);
@@ -692,13 +693,17 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     cfg.blockDim = dim3(Cfg::THREADS);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (c.split > 1) {  // launch early: producer and MMA warps run while Y is zeroed
+        pdl_attr(attr[1]);
+        cfg.numAttrs = 2;
+    }
     static const bool tracing = std::getenv("DB200_TC_TRACE") != nullptr;
     static unsigned long long* trace_buf = nullptr;
     if (tracing && !trace_buf && cudaMalloc(&trace_buf, 4096 * 16 * sizeof(unsigned long long)) != cudaSuccess)

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--graph", action="store_true", help="replay a captured CUDA graph of one launch")
+    ap.add_argument("--sketch", type=int, default=None)
     a = ap.parse_args()
     import torch
 
@@ -38,7 +39,7 @@ def main():
     else:
         y = torch.empty((L.get("b", 1), L["m"], L["n"]), device=dev)
         shape = {k: L[k] for k in ("b", "m", "n", "k") if k in L}
-    sk = sketches(L["op"], a.dtype)[0]
+    sk = a.sketch if a.sketch is not None else sketches(L["op"], a.dtype)[0]
     space = sketch_space(sk)
     vals = [int(v) for v in a.values.split(",")]
     p = (sk, tuple(space[d].index(v) for d, v in enumerate(vals)))
