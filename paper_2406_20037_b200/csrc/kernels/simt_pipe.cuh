@@ -160,18 +160,19 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
             if (chunksA % NT == 0 || e < chunksA) {
                 const int row = e / CPR, kl = (e % CPR) * VW;
                 const uint32_t dst = as + (uint32_t)(row * LDK + kl) * 4u;
-                const float* src = A;
-                int ok;
+                // branch-free: an out-of-image tap copies 0 bytes from the tensor base
+                int ok, off;
                 if constexpr (CONV) {
                     const int2 t = ktab[(k0 + kl) / VW];
                     const int h = ah0[i] + (t.y >> 16), w = aw0[i] + (t.y & 0xFFFF);
                     ok = (unsigned)h < (unsigned)p.H && (unsigned)w < (unsigned)p.W;
-                    if (ok) src = A + abase[i] + t.x;
+                    off = ok ? abase[i] + t.x : 0;
                 } else {
                     const int kk = kbeg + k0 + kl;
                     ok = ah0[i] == 0 && kk < p.K;
-                    if (ok) src = A + abase[i] + kk;
+                    off = ok ? abase[i] + kk : 0;
                 }
+                const float* src = A + off;
                 if constexpr (VW == 4) cp_async16(dst, src, ok ? 16 : 0);
                 else cp_async4(dst, src, ok ? 4 : 0);
             }
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
                 const int row = e / CPR, kl = (e % CPR) * VW;
                 const uint32_t dst = bs + (uint32_t)(row * LDK + kl) * 4u;
                 const bool ok = boff[i] >= 0 && kbeg + k0 + kl < p.K;
-                const float* src = ok ? B + boff[i] + k0 : B;
+                const float* src = B + (ok ? boff[i] + k0 : 0);
                 if constexpr (VW == 4) cp_async16(dst, src, ok ? 16 : 0);
                 else cp_async4(dst, src, ok ? 4 : 0);
             }
