@@ -77,10 +77,10 @@ def peaks():
 
 
 def traffic_evidence():
-    """DRAM traffic of the best r18.l1.3x3 schedule from the committed ncu --set full capture
-    (profiles/r1_ncu_simt_r18l1.raw.csv) next to that layer's algorithmic bytes."""
+    """DRAM traffic of a best r18.l1.3x3 schedule (cp.async sketch, split-K 8) from the committed
+    ncu --set full capture (profiles/r1_ncu_pipe5_r18l1.raw.csv) next to the layer's algorithmic bytes."""
     import csv
-    path = os.path.join(ROOT, "profiles", "r1_ncu_simt_r18l1.raw.csv")
+    path = os.path.join(ROOT, "profiles", "r1_ncu_pipe5_r18l1.raw.csv")
     try:
         rows = list(csv.reader(open(path)))
         d = {h: (v, u) for h, u, v in zip(rows[0], rows[1], rows[2])}
@@ -90,7 +90,7 @@ def traffic_evidence():
     except Exception:
         return None
     algo = 4 * (56 * 56 * 64 + 64 * 9 * 64 + 56 * 56 * 64)  # X + W + Y, fp32
-    return {"capture": "profiles/r1_ncu_simt_r18l1.raw.csv", "layer": "r18.l1.3x3", "dram_bytes": by,
+    return {"capture": "profiles/r1_ncu_pipe5_r18l1.raw.csv", "layer": "r18.l1.3x3", "dram_bytes": by,
             "algorithmic_bytes": algo, "ratio": by / algo}
 
 
