@@ -395,7 +395,7 @@ def main():
         peak = pk["bf16_tflops"]
         roofline = {"bound": "tensor", "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst) = {peak}"}
     roofline.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                     "kernel": "best 300+Droplet schedule per timed layer; sum F / sum median CUDA-event time"})
+                     "kernel": "best 300+Droplet schedule per timed layer; sum F / sum per-launch CUDA-event time (precise tier, R-M4)"})
     ev = traffic_evidence() if dtype == "f32" else None
     if ev:
         roofline["traffic_evidence"] = ev
