@@ -118,7 +118,14 @@ typedef struct {
     int32_t rank;
 } tuner_result;
 
-typedef enum { TUNER_DS_PLAIN = 0, TUNER_DS_GROW = 1 } tuner_ds_policy;
+/* Droplet policies (tuner_droplet): PLAIN = the paper's prose, P:297-304 (best improving
+ * neighbour of the +-1 ring, stop when none); GROW = after each ring move along u, probe the
+ * doubling ray x_prev + 2^j u as one batch (R-D9, north_star "grows its step"); RADIUS = when
+ * the +-1 ring holds no improving point, measure the axis-aligned ring at index distance
+ * r = 2, 3, ... until one does (move there, r back to 1) or no ring point is in range -- then
+ * converged, and the result is optimal along every axis line (R-D16: the original Droplet's
+ * speculation, which P:276-277 says the paper removed). */
+typedef enum { TUNER_DS_PLAIN = 0, TUNER_DS_GROW = 1, TUNER_DS_RADIUS = 2 } tuner_ds_policy;
 
 /* Host-side all-gather used when set (e.g. a gloo process group through the
  * Python binding): every rank contributes `bytes` bytes from `send`; `recv`

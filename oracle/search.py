@@ -108,13 +108,14 @@ class Space:
         """Every point once: sketches in order, each row-major (last knob fastest)."""
         return [self.point(g) for g in range(self.total)]
 
-    def ring(self, p: Point) -> List[Point]:
-        """The neighbourhood of P:292-294: +-1 index along each coordinate."""
+    def ring(self, p: Point, r: int = 1) -> List[Point]:
+        """The neighbourhood of P:292-294: +-1 index along each coordinate.  With r > 1 the
+        axis-aligned ring at index distance r (the expanding-radius reading, R-D16)."""
         s, idx = p
         cards = self.cards(s)
         out = []
         for d in range(len(idx)):
-            for delta in (-1, +1):
+            for delta in (-r, +r):
                 i = idx[d] + delta
                 if 0 <= i < cards[d]:
                     out.append((s, idx[:d] + (i,) + idx[d + 1:]))
@@ -287,7 +288,12 @@ class OracleTuner:
         unconverged (R-D13).  policy "grow" (R-D9, north_star "grows its step")
         after each ring move along u also probes x_prev + 2^j u (j = 1, 2, ...,
         clamped, until the clamp repeats) as one batch and accepts its points
-        in order while each is strictly better than the incumbent.
+        in order while each is strictly better than the incumbent.  policy "radius" (R-D16,
+        the original Droplet's speculation that P:276-277 says was removed): when the ring
+        holds no improving point, the axis-aligned ring at index distance r = 2, 3, ... is
+        measured instead (one batch and one round each) until a strictly better point is
+        found -- the search moves there and r returns to 1 -- or no ring point is in range
+        any more (converged: x is optimal along every axis line of its sketch).
         """
         if budget < 1:
             raise ValueError("budget must be >= 1")
@@ -314,8 +320,11 @@ class OracleTuner:
             room = budget - used
             return q[:room], len(q) > room
 
+        r = 1
         while True:
-            ring = self.space.ring(x)
+            ring = self.space.ring(x, r)
+            if r > 1 and not ring:  # R-D16: every axis line of x has been examined
+                return self._report(x, c, used, rounds, True, traj)
             q, trunc = new_batch(ring)
             if q:
                 self.measure(q)
@@ -327,7 +336,11 @@ class OracleTuner:
                     if best_p is None or self.memo[p] < best_c:
                         best_p, best_c = p, self.memo[p]
             if best_p is None or not better(best_p, x):
+                if policy == "radius" and not trunc:
+                    r += 1
+                    continue
                 return self._report(x, c, used, rounds, not trunc, traj)
+            r = 1
             prev = x
             x, c = best_p, best_c
             traj.append(x)

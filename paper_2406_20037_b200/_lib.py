@@ -20,7 +20,7 @@ OP = {"dense": 0, "batch_matmul": 1, "conv2d": 2, "depthwise_conv2d": 3}
 DTYPE = {"f32": 0, "bf16": 1}
 S_OK, S_INVALID, S_TIMEOUT, S_WRONG, S_LAUNCH_FAIL = range(5)
 SAMPLE_STATUS = ["ok", "invalid", "timeout", "wrong", "launch_fail"]
-POLICY = {"plain": 0, "grow": 1}
+POLICY = {"plain": 0, "grow": 1, "radius": 2}
 
 
 class Shape(C.Structure):

@@ -138,7 +138,7 @@ struct Tuner {
     tuner_point to_public(const Pt& p) const;
     void values_of(const Pt& p, int32_t* v) const;
     bool valid(const Pt& p) { return measurer->valid(p); }
-    void ring(const Pt& x, std::vector<Pt>& out) const;
+    void ring(const Pt& x, std::vector<Pt>& out, int r = 1) const;
     bool measured(const Pt& p) const { return memo.count(linear(p)) != 0; }
     double cost(const Pt& p) const { return history[memo.at(linear(p))].cost_ns; }
 

@@ -68,11 +68,13 @@ void Tuner::values_of(const Pt& p, int32_t* v) const {
 // Neighbourhood: one index step along one coordinate; no diagonals
 // (R-D7); out-of-range skipped, no wrap (R-D6); dimension-major, minus before
 // plus (R-D3).
-void Tuner::ring(const Pt& x, std::vector<Pt>& out) const {
+// the +-r axis-aligned ring (r = 1: the neighbourhood of P:292-294; r > 1: R-D16), dimension-
+// major, minus before plus, out-of-range indices skipped
+void Tuner::ring(const Pt& x, std::vector<Pt>& out, int r) const {
     out.clear();
     const SketchSpace& s = spaces[x.pos];
     for (int d = 0; d < x.n; ++d) {
-        for (int delta = -1; delta <= 1; delta += 2) {
+        for (int delta = -r; delta <= r; delta += 2 * r) {
             int i = x.idx[d] + delta;
             if (i < 0 || i >= (int)s.values[d].size()) continue;
             Pt q = x;
@@ -341,8 +343,10 @@ tuner_status Tuner::droplet(const Pt& start, int32_t budget, std::vector<Pt>& tr
         return n > q.size();
     };
     std::vector<Pt> nb, q, ray;
+    int r = 1;  // ring radius (RADIUS policy, R-D16)
     for (;;) {
-        ring(x, nb);
+        ring(x, nb, r);
+        if (r > 1 && nb.empty()) return finish(true);  // every axis line of x examined
         bool trunc = fresh(nb, q);
         if (!q.empty() && (st = measure_batch(q)) != TUNER_OK) return st;
         used += (int32_t)q.size();
@@ -354,7 +358,14 @@ tuner_status Tuner::droplet(const Pt& start, int32_t budget, std::vector<Pt>& tr
             double cp = cost(nb[i]);
             if (bi < 0 || cp < bc) { bi = (int)i; bc = cp; }
         }
-        if (bi < 0 || !better(nb[bi], x)) return finish(!trunc);
+        if (bi < 0 || !better(nb[bi], x)) {
+            if (opts.policy == TUNER_DS_RADIUS && !trunc) {
+                ++r;
+                continue;
+            }
+            return finish(!trunc);
+        }
+        r = 1;
         const Pt prev = x;
         x = nb[bi];
         c = bc;
@@ -490,7 +501,7 @@ extern "C" tuner_status tuner_create(int32_t op, const tuner_shape* shape, const
     if (!(t->opts.alpha >= 0.0 && t->opts.alpha < 1.0)) return fail(TUNER_EINVAL, "alpha must be in [0, 1)");
     if (t->opts.cost_samples && (t->opts.cost_nsamp < 1 || t->opts.cost_nsamp > kMaxSamples))
         return fail(TUNER_EINVAL, "cost_nsamp must be in [1, 16]");
-    if (t->opts.policy != TUNER_DS_PLAIN && t->opts.policy != TUNER_DS_GROW)
+    if (t->opts.policy != TUNER_DS_PLAIN && t->opts.policy != TUNER_DS_GROW && t->opts.policy != TUNER_DS_RADIUS)
         return fail(TUNER_EINVAL, "unknown Droplet policy");
     if (t->opts.world < 1) t->opts.world = 1;
     if (t->opts.rank < 0 || t->opts.rank >= t->opts.world) return fail(TUNER_EINVAL, "rank out of range");

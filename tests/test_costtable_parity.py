@@ -61,7 +61,7 @@ def run_product(sketches, table, seed, policy, n_sample, budget, max_batch, grou
     return out, t
 
 
-CASES = [(fam, seed, pol) for fam in FAMILIES for seed in range(6) for pol in ("plain", "grow")]
+CASES = [(fam, seed, pol) for fam in FAMILIES for seed in range(6) for pol in ("plain", "grow", "radius")]
 
 
 @pytest.mark.parametrize("family,seed,policy", CASES)

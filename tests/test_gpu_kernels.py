@@ -125,6 +125,43 @@ def test_simt_conv_exact_integer_inputs(sk):
         np.testing.assert_array_equal(yv, yo.astype(np.float32), err_msg=str(t.values(p)))
 
 
+@pytest.mark.parametrize("sk", [1, 8])
+def test_splitk_back_to_back_launches(sk):
+    # split-K zeroes Y with a kernel that releases the partial-sum kernel early (PDL); back-to-back
+    # launches (eager and replayed from a CUDA graph, as the timing harness does) must still leave
+    # exactly one launch's sum in Y: each zeroing waits for the previous launch to finish, and each
+    # partial-sum kernel waits for its zeroing before its first atomic
+    n, h, wd_, c, k, r, s = 1, 14, 14, 64, 64, 3, 3
+    x, w = tensors([(n, h, wd_, c), (k, r, s, c)], 21)
+    yo, ao = oc.conv2d(x, w, (1, 1), (1, 1))
+    xd, wdd = to_dev(x, w)
+    y = torch.empty(yo.shape, device=dev())
+    shape = {"N": n, "H": h, "W": wd_, "C": c, "K": k, "R": r, "S": s, "stride": (1, 1), "pad": (1, 1)}
+    space = sketch_space(sk)
+    t = Tuner("conv2d", shape, spaces=[(sk, space)], x=xd, w=wdd, y=y)
+    pts = [p for p in all_points(sk) if t.valid(p) and t.values(p)[7] >= 4]
+    assert pts
+    st = torch.cuda.Stream()
+    for p in random.Random(5).sample(pts, 12):
+        y.fill_(float("nan"))
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            for _ in range(20):
+                t.run(p, xd, wdd, y, stream=st)
+        st.synchronize()
+        assert on.max_rel_err(y.cpu().numpy(), yo, ao) <= on.TOL_F32, ("eager", t.values(p))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(8):
+                t.run(p, xd, wdd, y, stream=st)
+        y.fill_(float("nan"))
+        torch.cuda.synchronize()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        assert on.max_rel_err(y.cpu().numpy(), yo, ao) <= on.TOL_F32, ("graph", t.values(p))
+
+
 def test_naive_reference_vs_oracle():
     x, w = tensors([(2, 10, 9, 5), (7, 3, 3, 5)], 3)
     yo, ao = oc.conv2d(x, w, (2, 1), (1, 1))

@@ -95,7 +95,7 @@ def test_droplet_example_golden(policy):
         assert sp.values(rep["best"]) == exp["best_values"]
 
 
-@pytest.mark.parametrize("policy", ["plain", "grow"])
+@pytest.mark.parametrize("policy", ["plain", "grow", "radius"])
 def test_droplet_separable_convex_closed_form(policy):
     # cost sum (v_i - 3)^2 on {0..9}^4 from (0,0,0,0) -> (3,3,3,3)
     sp = Space([[list(range(10))] * 4])
@@ -116,7 +116,7 @@ def random_table(rng, dims, inv=0.1):
     return cards, tab
 
 
-@pytest.mark.parametrize("policy", ["plain", "grow"])
+@pytest.mark.parametrize("policy", ["plain", "grow", "radius"])
 def test_droplet_invariants_vs_brute_force(policy):
     rng = random.Random(7)
     checked = 0
@@ -143,10 +143,21 @@ def test_droplet_invariants_vs_brute_force(policy):
         if policy == "plain":
             for a, b in zip(rep["traj"], rep["traj"][1:]):
                 assert b in sp.ring(a)
+        if policy == "radius":
+            # every move is along one axis; a converged result is optimal along every axis
+            # line through it (R-D16): brute force over each line
+            for a, b in zip(rep["traj"], rep["traj"][1:]):
+                assert sum(i != j for i, j in zip(a[1], b[1])) == 1
+            if rep["converged"]:
+                c0 = cost(rep["best"])
+                for d in range(len(cards)):
+                    for i in range(cards[d]):
+                        q = (0, rep["best"][1][:d] + (i,) + rep["best"][1][d + 1:])
+                        assert not valid(q) or cost(q) >= c0
     assert checked > 200
 
 
-@pytest.mark.parametrize("policy", ["plain", "grow"])
+@pytest.mark.parametrize("policy", ["plain", "grow", "radius"])
 def test_droplet_unimodal_reaches_global(policy):
     rng = random.Random(3)
     for _ in range(60):
@@ -161,6 +172,47 @@ def test_droplet_unimodal_reaches_global(policy):
         t = OracleTuner(sp, cost, lambda p: True)
         rep = t.droplet(start, 10 ** 5, policy)
         assert rep["best"] == bp and rep["converged"]
+
+
+def test_radius_escapes_a_ring_trap_hand_traced():
+    # 1-D table [5, 4, 6, 1, 7] from index 0 (R-D16).  PLAIN: ring {1}: 4 < 5 -> move; ring
+    # {0, 2} = {5, 6}: no move -> converged at 1 (cost 4), 3 trials, 2 rounds.  RADIUS: at 1, ring
+    # r=2 = {3} (index -1 out of range): 1 < 4 -> move to 3, r = 1; ring {2, 4} = {6, 7} (2
+    # memoised): no; r=2 {1} memoised: no; r=3 {0} memoised: no; r=4: nothing in range ->
+    # converged at 3 (cost 1): trials 1 + 1 + 1 + 1 + 1 = 5 (0, 1, 2, 3, 4), rounds 2 + 1 + 3 = 6
+    tab = [5.0, 4.0, 6.0, 1.0, 7.0]
+    sp = Space([[list(range(5))]])
+    cost, valid = table_cost(sp, tab)
+    t = OracleTuner(sp, cost, valid)
+    rp = t.droplet((0, (0,)), 100, "plain")
+    assert rp["best"] == (0, (1,)) and rp["trials_used"] == 3 and rp["rounds"] == 2 and rp["converged"]
+    t = OracleTuner(sp, cost, valid)
+    rr = t.droplet((0, (0,)), 100, "radius")
+    assert [p[1][0] for p in rr["traj"]] == [0, 1, 3]
+    assert rr["best_cost"] == 1.0 and rr["trials_used"] == 5 and rr["rounds"] == 6 and rr["converged"]
+
+
+def test_radius_equals_plain_when_plain_ends_axis_optimal():
+    # the radius-1 phase is PLAIN verbatim: whenever PLAIN's converged point is already optimal
+    # along every axis line, RADIUS takes the same trajectory and only adds the outer rings
+    rng = random.Random(13)
+    same = 0
+    for _ in range(400):
+        cards, tab = random_table(rng, rng.randint(1, 3), inv=0.0)
+        sp = Space([[list(range(c)) for c in cards]])
+        cost, valid = table_cost(sp, tab)
+        start = (0, tuple(rng.randrange(c) for c in cards))
+        rp = OracleTuner(sp, cost, valid).droplet(start, 10 ** 4, "plain")
+        rr = OracleTuner(sp, cost, valid).droplet(start, 10 ** 4, "radius")
+        c0 = cost(rp["best"])
+        axis_opt = all(cost((0, rp["best"][1][:d] + (i,) + rp["best"][1][d + 1:])) >= c0
+                       for d in range(len(cards)) for i in range(cards[d]))
+        if axis_opt:
+            assert rr["traj"] == rp["traj"] and rr["trials_used"] >= rp["trials_used"]
+            same += 1
+        else:
+            assert rr["best_cost"] < rp["best_cost"]  # it escaped PLAIN's ring trap
+    assert same > 100
 
 
 def test_grow_within_100_trials_on_convex():
