@@ -176,13 +176,14 @@ def test_naive_reference_vs_oracle():
     np.testing.assert_allclose(ar.cpu().numpy(), ao.astype(np.float32), rtol=1e-6)
 
 
-def test_harness_sample_droplet_and_replay():
+@pytest.mark.parametrize("policy", ["grow", "radius"])
+def test_harness_sample_droplet_and_replay(policy):
     from oracle.search import OracleTuner, Space
     m = n = k = 256
     x, w, yo, ao = gemm_case(1, m, n, k, "uniform", 11)
     xd, wd = to_dev(x, w)
     y = torch.empty(m, n, device=dev())
-    t = Tuner("dense", {"m": m, "n": n, "k": k}, x=xd, w=wd, y=y, seed=3)
+    t = Tuner("dense", {"m": m, "n": n, "k": k}, x=xd, w=wd, y=y, seed=3, policy=policy)
     l0 = global_launch_count()
     smp = t.sample(64)
     assert len(smp) == 64
@@ -207,7 +208,7 @@ def test_harness_sample_droplet_and_replay():
         return log[to_l(p)]
     ot = OracleTuner(sp, cost, lambda p: to_l(p) in log)
     ot.measure([to_o(p) for p in pre])
-    orep = ot.droplet(to_o(b.point), 100, "grow")
+    orep = ot.droplet(to_o(b.point), 100, policy)
     assert [to_l(p) for p in orep["traj"]] == [(p[0], tuple(p[1])) for p in rep["traj"]]
     assert orep["trials_used"] == rep["trials_used"] and orep["converged"] == rep["converged"]
     # the chosen schedule really computes the layer
