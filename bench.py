@@ -253,8 +253,8 @@ def main():
         # sketch rule (Ansor's rules are hardware-dependent): a bf16 conv is tuned
         # on the tcgen05 sketch when TMA can address it (C % 8 == 0), else on the SIMT one
         if dtype == "bf16" and L["op"] == "conv2d":
-            sk = 3 if L["C"] % 8 == 0 else 4
-            return [(sk, sketch_space(sk))]
+            sks = [3 if L["C"] % 8 == 0 else 4] + ([10] if L["C"] <= 16 else [])  # + direct conv (stems)
+            return [(sk, sketch_space(sk)) for sk in sks]
         return None
 
     def tune_layer(li, seed, e2e=False, pinned=None):

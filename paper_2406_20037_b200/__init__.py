@@ -15,3 +15,5 @@ SK_SIMT_DWCONV_F32 = 5
 SK_SIMT_DWCONV_BF16 = 6
 SK_SIMT_PIPE_GEMM_F32 = 7
 SK_SIMT_PIPE_CONV_F32 = 8
+SK_SIMT_DIRECT_CONV_F32 = 9
+SK_SIMT_DIRECT_CONV_BF16 = 10

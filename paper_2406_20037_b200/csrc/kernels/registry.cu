@@ -16,6 +16,7 @@ DECL_PIPE(0, 16) DECL_PIPE(0, 32) DECL_PIPE(0, 64) DECL_PIPE(0, 128) DECL_PIPE(1
 void register_tc_gemm();
 void register_simt_bf16_conv();
 void register_dwconv();
+void register_direct_conv();
 
 static std::unordered_map<uint64_t, LaunchFn>& table() {
     static std::unordered_map<uint64_t, LaunchFn> t;
@@ -31,6 +32,7 @@ static void init_all() {
     register_tc_gemm();
     register_simt_bf16_conv();
     register_dwconv();
+    register_direct_conv();
 }
 
 uint64_t kernel_key(int32_t sketch, int a, int b, int c, int d, int e) {

@@ -17,7 +17,9 @@ enum SketchId : int32_t {
     SK_SIMT_DWCONV_BF16 = 6,
     SK_SIMT_PIPE_GEMM_F32 = 7,
     SK_SIMT_PIPE_CONV_F32 = 8,
-    SK_COUNT = 9
+    SK_SIMT_DIRECT_CONV_F32 = 9,
+    SK_SIMT_DIRECT_CONV_BF16 = 10,
+    SK_COUNT = 11
 };
 
 // depthwise sketch: shared-memory bytes of a CTA (filters [R*S][ctv] + input window
@@ -44,6 +46,13 @@ inline size_t pipe_smem_bytes(int bm, int bn, int bk, int kw, int stages, bool c
     return (pipe > red ? pipe : red) + ktab;
 }
 constexpr int kPipeMaxSlots = 8;  // cp.async slots per thread per operand
+
+// direct conv sketches: filters [R*S*C][BKC] fp32, or (EPI 1) the [PX][BKC + 4] output tile if larger
+inline size_t direct_smem_bytes(int rsc, int bkc, int px, int epi) {
+    const size_t wb = (size_t)rsc * bkc * 4;
+    const size_t yb = epi ? (size_t)px * (bkc + 4) * 4 : 0;
+    return wb > yb ? wb : yb;
+}
 
 struct ShapeInfo {  // derived GEMM view of the problem (depthwise: M = n*p*q, N = c, K = r*s)
     int32_t op, dtype;

@@ -61,6 +61,15 @@ static std::vector<SketchDesc> build_catalogue() {
                                                            {1, 2},            {1, 2, 4, 8, 16}};
     c.push_back({SK_SIMT_IGEMM_CONV_BF16, "simt_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, simt_names,
                  simt16_vals});
+    // direct conv (SURVEY §8(d).1 `simt_direct_conv`) for few-input-channel layers: KT output
+    // channels per thread (compile-time), PX pixels x BKC channels per CTA, EPI 0 per-thread
+    // stores / 1 tile staged through shared memory (runtime)
+    const std::vector<const char*> dc_names = {"KT", "PX", "BKC", "EPI"};
+    const std::vector<std::vector<int32_t>> dc_vals = {{4, 8, 16, 32, 64}, {32, 64, 128, 256}, {16, 32, 64, 128},
+                                                       {0, 1}};
+    c.push_back({SK_SIMT_DIRECT_CONV_F32, "simt_direct_conv_f32", 1 << TUNER_OP_CONV2D, TUNER_F32, dc_names, dc_vals});
+    c.push_back({SK_SIMT_DIRECT_CONV_BF16, "simt_direct_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, dc_names,
+                 dc_vals});
     // depthwise conv: VEC channels per thread (vector loads along C), CT
     // threads across channels, TQ output columns per thread, QT x PT threads across
     // output columns / rows, TP output rows per thread, ALG = 0 register window,
@@ -165,6 +174,17 @@ static bool pipe_valid(const ShapeInfo& sh, const int32_t* v) {
     return true;
 }
 
+static bool direct_valid(const ShapeInfo& sh, const int32_t* v) {
+    const int kt = v[0], px = v[1], bkc = v[2], epi = v[3];
+    if (sh.c > 16) return false;  // sketch rule: the direct loop nest is for few-channel stems
+    if (kt > bkc || bkc % kt) return false;
+    const int threads = px * (bkc / kt);
+    if (threads < 32 || threads > 1024) return false;
+    if (direct_smem_bytes((int)(sh.r * sh.s * sh.c), bkc, px, epi) > 227 * 1024) return false;
+    if ((sh.k + bkc - 1) / bkc > 65535) return false;
+    return true;
+}
+
 static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
     const int bm = v[0], bn = v[1], bk = v[2], stages = v[3], split = v[4];
     const int sched = sh.op == TUNER_OP_CONV2D ? v[6] : v[5];
@@ -223,6 +243,8 @@ bool sketch_valid(int32_t id, const ShapeInfo& sh, const int32_t* v) {
         case SK_SIMT_IGEMM_CONV_BF16: return simt_valid(sh, v);
         case SK_SIMT_PIPE_GEMM_F32:
         case SK_SIMT_PIPE_CONV_F32: return pipe_valid(sh, v);
+        case SK_SIMT_DIRECT_CONV_F32:
+        case SK_SIMT_DIRECT_CONV_BF16: return direct_valid(sh, v);
         case SK_TC_GEMM_BF16:
         case SK_TC_IGEMM_CONV_BF16: return tc_valid(sh, v);
         case SK_SIMT_DWCONV_F32:

@@ -42,7 +42,8 @@ def test_struct_sizes_match_c_layout():
 def test_catalogue():
     assert sketches("dense", "f32") == [0, 7]
     assert sketches("batch_matmul", "f32") == [0, 7]
-    assert sketches("conv2d", "f32") == [1, 8]
+    assert sketches("conv2d", "f32") == [1, 8, 9]
+    assert sketches("conv2d", "bf16") == [3, 4, 10]
     assert sketches("dense", "bf16") == [2]
     assert sketch_name(0) == "simt_gemm_f32"
     assert knob_names(0) == ["BM", "BN", "BK", "TT", "UNROLL", "VEC", "STAGES", "SPLIT_K"]
@@ -52,6 +53,8 @@ def test_catalogue():
     assert knob_names(3) == ["BM", "BN", "BK", "STAGES", "SPLIT_K", "TILE_Q", "SCHED", "RASTER"]
     assert sketch_name(8) == "simt_pipe_conv_f32"
     assert knob_names(8) == ["BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K"]
+    assert sketch_name(10) == "simt_direct_conv_bf16"
+    assert knob_names(9) == ["KT", "PX", "BKC", "EPI"]
     assert sketch_name(99) is None
 
 

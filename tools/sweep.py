@@ -80,8 +80,8 @@ def main():
             y = torch.empty(yshape, device=dev)
             spaces = None
             if a.dtype == "bf16" and L["op"] == "conv2d":
-                sk = 3 if L["C"] % 8 == 0 else 4
-                spaces = [(sk, sketch_space(sk))]
+                sks = [3 if L["C"] % 8 == 0 else 4] + ([10] if L["C"] <= 16 else [])  # + direct conv (stems)
+                spaces = [(sk, sketch_space(sk)) for sk in sks]
             fl = layer_flops(L)
             rec = {"model": mname, "layer": L["name"], "op": L["op"], "count": L["count"], "gflop": fl / 1e9,
                    "shape": {k: v for k, v in L.items() if k not in ("name", "count", "op")}}
