@@ -93,12 +93,12 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
             rk.sched = v[6];
             rk.raster = v[7];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[5]));
-        case SK_SIMT_DIRECT_CONV_F32:  // KT (compiled) | PX, BKC, EPI
+        case SK_SIMT_DIRECT_CONV_F32:  // KT, TP (compiled) | PX, BKC, EPI
         case SK_SIMT_DIRECT_CONV_BF16:
-            rk.dims[0] = v[1];
-            rk.dims[1] = v[2];
-            rk.dims[2] = v[3];
-            return registry_find(kernel_key(sk, v[0], 0, 0, 0, 0));
+            rk.dims[0] = v[2];
+            rk.dims[1] = v[3];
+            rk.dims[2] = v[4];
+            return registry_find(kernel_key(sk, v[0], v[1], 0, 0, 0));
         case SK_SIMT_DWCONV_F32:
         case SK_SIMT_DWCONV_BF16:  // VEC, CT, TQ, QT, PT, TP, ALG
             rk.dims[0] = v[1];

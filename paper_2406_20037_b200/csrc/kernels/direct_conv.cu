@@ -3,14 +3,15 @@
 // view, for layers with few input channels (C <= 16: the RGB stems of VGG / AlexNet / ResNet),
 // where an implicit GEMM has a reduction of only C*R*S = 27..363 and its gathers dominate.
 //
-// Schedule: a CTA owns PX consecutive output pixels (NPQ order) x BKC output channels; the
-// CTA's filters are staged once in shared memory as [R*S*C][BKC] fp32; each thread owns one
-// pixel and KT consecutive channels, walks the taps (r, s, c) reading each input element once
-// (zero outside the image) and updates KT accumulators with FFMA2 (broadcast input value x
-// pairs of filter values, the filter row read as float4 broadcasts: every lane of a warp
-// shares its channel group).  Epilogue: EPI 0 = each thread stores its KT channels (float4);
-// EPI 1 = the PX x BKC tile is staged through shared memory and written as contiguous rows.
-// Annotations: KT (compile-time), PX, BKC, EPI (runtime).  fp32 accumulation, fp32 output.
+// Schedule: a CTA owns PX*TP consecutive output pixels (NPQ order) x BKC output channels; the
+// CTA's filters are staged once in shared memory as [R*S*C][BKC] fp32; each thread owns TP
+// pixels (PX apart, so a warp's lanes stay on consecutive pixels) and KT consecutive channels,
+// walks the taps (r, s, c) reading each input element once (zero outside the image) and updates
+// TP x KT accumulators with FFMA2 (broadcast input value x pairs of filter values; each float4
+// filter broadcast -- every lane of a warp shares its channel group -- feeds 2*TP FFMA2).
+// Epilogue: EPI 0 = each thread stores its KT channels per pixel (float4); EPI 1 = the tile is
+// staged through shared memory and written as contiguous rows.
+// Annotations: KT, TP (compile-time), PX, BKC, EPI (runtime).  fp32 accumulation, fp32 output.
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -39,14 +40,14 @@ __device__ __forceinline__ float2 dffma2(float a, float b0, float b1, float2 c) 
     return r;
 }
 
-template <typename TIn, int KT>
-__global__ void __launch_bounds__(1024) direct_conv_kernel(const DirectParams p) {
+template <typename TIn, int KT, int TP>
+__global__ void __launch_bounds__(direct_max_threads(KT, TP)) direct_conv_kernel(const DirectParams p) {
     extern __shared__ __align__(16) float dsm[];
     const int RSC = p.R * p.S * p.C, BKC = p.bkc, PX = p.px;
     float* wsm = dsm;  // [RSC][BKC]
     const int tid = threadIdx.x;
     const int pxl = tid % PX, kg = tid / PX;
-    const int m0 = blockIdx.x * PX, k0 = blockIdx.y * BKC;
+    const int m0 = blockIdx.x * PX * TP, k0 = blockIdx.y * BKC;
     const TIn* __restrict__ X = (const TIn*)p.X;
     const TIn* __restrict__ Wt = (const TIn*)p.Wt;
 
@@ -57,36 +58,53 @@ __global__ void __launch_bounds__(1024) direct_conv_kernel(const DirectParams p)
     }
     __syncthreads();
 
-    const int m = m0 + pxl;
-    const bool live = m < p.M;
-    int n = 0, h0 = 0, w0 = 0;
-    if (live) {
-        const int q = m % p.Q, t = m / p.Q, pp = t % p.P;
-        n = t / p.P;
-        h0 = pp * p.sh - p.ph;
-        w0 = q * p.sw - p.pw;
-    }
-    float2 acc[KT / 2];
+    bool live[TP];
+    int nb[TP], h0[TP], w0[TP];
+    bool any = false;
 #pragma unroll
-    for (int j = 0; j < KT / 2; ++j) acc[j] = make_float2(0.f, 0.f);
+    for (int u = 0; u < TP; ++u) {
+        const int m = m0 + pxl + u * PX;
+        live[u] = m < p.M;
+        any |= live[u];
+        nb[u] = 0; h0[u] = -(1 << 29); w0[u] = 0;  // a dead pixel reads nothing (h out of range)
+        if (live[u]) {
+            const int q = m % p.Q, t = m / p.Q, pp = t % p.P;
+            nb[u] = (t / p.P) * p.H;
+            h0[u] = pp * p.sh - p.ph;
+            w0[u] = q * p.sw - p.pw;
+        }
+    }
+    float2 acc[TP][KT / 2];
+#pragma unroll
+    for (int u = 0; u < TP; ++u)
+#pragma unroll
+        for (int j = 0; j < KT / 2; ++j) acc[u][j] = make_float2(0.f, 0.f);
     const float* wk = wsm + kg * KT;
-    if (live) {
+    if (any) {
         for (int r = 0; r < p.R; ++r) {
-            const int h = h0 + r * p.dh;
-            const bool hok = (unsigned)h < (unsigned)p.H;
             for (int s = 0; s < p.S; ++s) {
-                const int w = w0 + s * p.dw;
-                const bool ok = hok && (unsigned)w < (unsigned)p.W;
-                const TIn* xp = X + (((long long)n * p.H + (ok ? h : 0)) * p.W + (ok ? w : 0)) * p.C;
+                bool ok[TP];
+                const TIn* xp[TP];
+#pragma unroll
+                for (int u = 0; u < TP; ++u) {
+                    const int h = h0[u] + r * p.dh, w = w0[u] + s * p.dw;
+                    ok[u] = (unsigned)h < (unsigned)p.H && (unsigned)w < (unsigned)p.W;
+                    xp[u] = X + ((long long)(nb[u] + (ok[u] ? h : 0)) * p.W + (ok[u] ? w : 0)) * p.C;
+                }
                 const float* wr = wk + (r * p.S + s) * p.C * BKC;
                 for (int c = 0; c < p.C; ++c) {
-                    const float x = ok ? dld(xp + c) : 0.f;
+                    float x[TP];
+#pragma unroll
+                    for (int u = 0; u < TP; ++u) x[u] = ok[u] ? dld(xp[u] + c) : 0.f;
                     const float* wc = wr + c * BKC;
 #pragma unroll
                     for (int j = 0; j < KT / 4; ++j) {
                         const float4 w4 = *reinterpret_cast<const float4*>(wc + 4 * j);
-                        acc[2 * j] = dffma2(x, w4.x, w4.y, acc[2 * j]);
-                        acc[2 * j + 1] = dffma2(x, w4.z, w4.w, acc[2 * j + 1]);
+#pragma unroll
+                        for (int u = 0; u < TP; ++u) {
+                            acc[u][2 * j] = dffma2(x[u], w4.x, w4.y, acc[u][2 * j]);
+                            acc[u][2 * j + 1] = dffma2(x[u], w4.z, w4.w, acc[u][2 * j + 1]);
+                        }
                     }
                 }
             }
@@ -95,35 +113,40 @@ __global__ void __launch_bounds__(1024) direct_conv_kernel(const DirectParams p)
 
     const int kb = k0 + kg * KT;  // this thread's first channel
     if (p.epi == 0) {
-        if (!live) return;
-        float* yp = p.Y + (long long)m * p.K + kb;
         const bool vec = (p.K % 4) == 0;
 #pragma unroll
-        for (int j = 0; j < KT / 4; ++j) {
-            const float4 v = make_float4(acc[2 * j].x, acc[2 * j].y, acc[2 * j + 1].x, acc[2 * j + 1].y);
-            if (vec && kb + 4 * j + 3 < p.K) {
-                *reinterpret_cast<float4*>(yp + 4 * j) = v;
-            } else {
-                const float vv[4] = {v.x, v.y, v.z, v.w};
+        for (int u = 0; u < TP; ++u) {
+            if (!live[u]) continue;
+            float* yp = p.Y + (long long)(m0 + pxl + u * PX) * p.K + kb;
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (kb + 4 * j + u < p.K) yp[4 * j + u] = vv[u];
+            for (int j = 0; j < KT / 4; ++j) {
+                const float4 v = make_float4(acc[u][2 * j].x, acc[u][2 * j].y, acc[u][2 * j + 1].x, acc[u][2 * j + 1].y);
+                if (vec && kb + 4 * j + 3 < p.K) {
+                    *reinterpret_cast<float4*>(yp + 4 * j) = v;
+                } else {
+                    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (kb + 4 * j + e < p.K) yp[4 * j + e] = vv[e];
+                }
             }
         }
         return;
     }
-    // EPI 1: the tile through shared memory ([PX][BKC + 4]), then contiguous row stores
+    // EPI 1: the tile through shared memory ([PX * TP][BKC + 4]), then contiguous row stores
     __syncthreads();  // filters no longer needed: the staging tile reuses their space
     const int LD = BKC + 4;
     float* ysm = dsm;
 #pragma unroll
-    for (int j = 0; j < KT / 4; ++j)
-        *reinterpret_cast<float4*>(ysm + pxl * LD + kg * KT + 4 * j) =
-            make_float4(acc[2 * j].x, acc[2 * j].y, acc[2 * j + 1].x, acc[2 * j + 1].y);
+    for (int u = 0; u < TP; ++u)
+#pragma unroll
+        for (int j = 0; j < KT / 4; ++j)
+            *reinterpret_cast<float4*>(ysm + (pxl + u * PX) * LD + kg * KT + 4 * j) =
+                make_float4(acc[u][2 * j].x, acc[u][2 * j].y, acc[u][2 * j + 1].x, acc[u][2 * j + 1].y);
     __syncthreads();
     const int c4 = BKC / 4;
     const bool vec = (p.K % 4) == 0;
-    for (int e = tid; e < PX * c4; e += blockDim.x) {
+    for (int e = tid; e < PX * TP * c4; e += blockDim.x) {
         const int row = e / c4, col = (e - row * c4) * 4;
         const int mm = m0 + row, kk = k0 + col;
         if (mm >= p.M || kk >= p.K) continue;
@@ -139,9 +162,9 @@ __global__ void __launch_bounds__(1024) direct_conv_kernel(const DirectParams p)
     }
 }
 
-template <typename TIn, int KT>
+template <typename TIn, int KT, int TP>
 cudaError_t direct_launch(const LaunchCtx& c) {
-    auto kern = direct_conv_kernel<TIn, KT>;
+    auto kern = direct_conv_kernel<TIn, KT, TP>;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -155,25 +178,33 @@ cudaError_t direct_launch(const LaunchCtx& c) {
     p.P = (int)s.p; p.Q = (int)s.q; p.sh = s.sh; p.sw = s.sw; p.ph = s.ph; p.pw = s.pw; p.dh = s.dh; p.dw = s.dw;
     p.M = (int)s.M;
     p.px = c.dims[0]; p.bkc = c.dims[1]; p.epi = c.dims[2];
-    const size_t smem = direct_smem_bytes((int)(s.r * s.s * s.c), p.bkc, p.px, p.epi);
-    dim3 grid((unsigned)((s.M + p.px - 1) / p.px), (unsigned)((s.k + p.bkc - 1) / p.bkc));
+    const size_t smem = direct_smem_bytes((int)(s.r * s.s * s.c), p.bkc, p.px * TP, p.epi);
+    dim3 grid((unsigned)((s.M + p.px * TP - 1) / (p.px * TP)), (unsigned)((s.k + p.bkc - 1) / p.bkc));
     kern<<<grid, (unsigned)(p.px * (p.bkc / KT)), smem, c.stream>>>(p);
     count_launches(1);
     return cudaGetLastError();
 }
 
-template <int KT>
+template <int KT, int TP>
 void direct_register() {
-    registry_add(kernel_key(SK_SIMT_DIRECT_CONV_F32, KT, 0, 0, 0, 0), &direct_launch<float, KT>);
-    registry_add(kernel_key(SK_SIMT_DIRECT_CONV_BF16, KT, 0, 0, 0, 0), &direct_launch<__nv_bfloat16, KT>);
+    if constexpr (KT * TP <= 64) {  // accumulators per thread (register budget; the validity rule)
+        registry_add(kernel_key(SK_SIMT_DIRECT_CONV_F32, KT, TP, 0, 0, 0), &direct_launch<float, KT, TP>);
+        registry_add(kernel_key(SK_SIMT_DIRECT_CONV_BF16, KT, TP, 0, 0, 0), &direct_launch<__nv_bfloat16, KT, TP>);
+    }
+}
+template <int KT>
+void direct_register_tp() {
+    direct_register<KT, 1>();
+    direct_register<KT, 2>();
+    direct_register<KT, 4>();
 }
 
 void register_direct_conv() {
-    direct_register<4>();
-    direct_register<8>();
-    direct_register<16>();
-    direct_register<32>();
-    direct_register<64>();
+    direct_register_tp<4>();
+    direct_register_tp<8>();
+    direct_register_tp<16>();
+    direct_register_tp<32>();
+    direct_register_tp<64>();
 }
 
 }  // namespace db200

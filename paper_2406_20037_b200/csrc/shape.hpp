@@ -47,6 +47,9 @@ inline size_t pipe_smem_bytes(int bm, int bn, int bk, int kw, int stages, bool c
 }
 constexpr int kPipeMaxSlots = 8;  // cp.async slots per thread per operand
 
+// direct conv sketches: the block-size bound of an instantiation (its accumulators need
+// registers: KT*TP floats per thread) -- the kernel's __launch_bounds__ and the validity rule
+constexpr int direct_max_threads(int kt, int tp) { return kt * tp >= 64 ? 256 : (kt * tp >= 32 ? 512 : 1024); }
 // direct conv sketches: filters [R*S*C][BKC] fp32, or (EPI 1) the [PX][BKC + 4] output tile if larger
 inline size_t direct_smem_bytes(int rsc, int bkc, int px, int epi) {
     const size_t wb = (size_t)rsc * bkc * 4;

@@ -64,9 +64,9 @@ static std::vector<SketchDesc> build_catalogue() {
     // direct conv (SURVEY §8(d).1 `simt_direct_conv`) for few-input-channel layers: KT output
     // channels per thread (compile-time), PX pixels x BKC channels per CTA, EPI 0 per-thread
     // stores / 1 tile staged through shared memory (runtime)
-    const std::vector<const char*> dc_names = {"KT", "PX", "BKC", "EPI"};
-    const std::vector<std::vector<int32_t>> dc_vals = {{4, 8, 16, 32, 64}, {32, 64, 128, 256}, {16, 32, 64, 128},
-                                                       {0, 1}};
+    const std::vector<const char*> dc_names = {"KT", "TP", "PX", "BKC", "EPI"};
+    const std::vector<std::vector<int32_t>> dc_vals = {{4, 8, 16, 32, 64}, {1, 2, 4}, {32, 64, 128, 256},
+                                                       {16, 32, 64, 128}, {0, 1}};
     c.push_back({SK_SIMT_DIRECT_CONV_F32, "simt_direct_conv_f32", 1 << TUNER_OP_CONV2D, TUNER_F32, dc_names, dc_vals});
     c.push_back({SK_SIMT_DIRECT_CONV_BF16, "simt_direct_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, dc_names,
                  dc_vals});
@@ -175,12 +175,12 @@ static bool pipe_valid(const ShapeInfo& sh, const int32_t* v) {
 }
 
 static bool direct_valid(const ShapeInfo& sh, const int32_t* v) {
-    const int kt = v[0], px = v[1], bkc = v[2], epi = v[3];
+    const int kt = v[0], tp = v[1], px = v[2], bkc = v[3], epi = v[4];
     if (sh.c > 16) return false;  // sketch rule: the direct loop nest is for few-channel stems
-    if (kt > bkc || bkc % kt) return false;
+    if (kt > bkc || bkc % kt || kt * tp > 64) return false;
     const int threads = px * (bkc / kt);
-    if (threads < 32 || threads > 1024) return false;
-    if (direct_smem_bytes((int)(sh.r * sh.s * sh.c), bkc, px, epi) > 227 * 1024) return false;
+    if (threads < 32 || threads > direct_max_threads(kt, tp)) return false;
+    if (direct_smem_bytes((int)(sh.r * sh.s * sh.c), bkc, px * tp, epi) > 227 * 1024) return false;
     if ((sh.k + bkc - 1) / bkc > 65535) return false;
     return true;
 }

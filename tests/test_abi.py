@@ -54,7 +54,7 @@ def test_catalogue():
     assert sketch_name(8) == "simt_pipe_conv_f32"
     assert knob_names(8) == ["BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K"]
     assert sketch_name(10) == "simt_direct_conv_bf16"
-    assert knob_names(9) == ["KT", "PX", "BKC", "EPI"]
+    assert knob_names(9) == ["KT", "TP", "PX", "BKC", "EPI"]
     assert sketch_name(99) is None
 
 
