@@ -198,7 +198,15 @@ void tuner_opts_default(tuner_opts* o);
 /* Sketch catalogue.  tuner_sketches lists the sketch ids that implement (op,
  * dtype); tuner_sketch_space returns a sketch's full supported knob space
  * (card[TUNER_MAX_KNOBS], values[TUNER_MAX_KNOBS*TUNER_MAX_VALUES]);
- * tuner_knob_name returns a static string ("BM", "SPLIT_K", ...) or NULL. */
+ * tuner_knob_name returns a static string ("BM", "SPLIT_K", ...) or NULL.
+ * Sketch ids (a sketch = one fixed sequence of transformations of the loop nest,
+ * Def. 2.1; its knobs are the annotations):
+ *   0 simt_gemm_f32 / 1 simt_igemm_conv_f32     register-staged SIMT tiles (fp32)
+ *   7 simt_pipe_gemm_f32 / 8 simt_pipe_conv_f32 cp.async multistage SIMT tiles (fp32)
+ *   9 simt_direct_conv_f32 / 10 ..._bf16        direct conv, C <= 16 stems
+ *   2 tc_gemm_bf16 / 3 tc_igemm_conv_bf16       tcgen05 / TMEM / TMA (bf16 in, fp32 out)
+ *   4 simt_igemm_conv_bf16                      SIMT implicit GEMM on bf16 inputs
+ *   5 simt_dwconv_f32 / 6 simt_dwconv_bf16      depthwise conv */
 tuner_status tuner_sketches(int32_t op, int32_t dtype, int32_t* ids, int32_t cap, int32_t* n_out);
 tuner_status tuner_sketch_space(int32_t sketch, int32_t* nknobs, int32_t* card, int32_t* values);
 const char* tuner_sketch_name(int32_t sketch);
