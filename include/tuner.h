@@ -306,6 +306,15 @@ const char* tuner_last_error(void);
 /* Total candidate-kernel launches by this process (all handles). */
 int64_t tuner_global_launch_count(void);
 
+/* FP32 pipe peak microbenchmark (BASELINE.md §2 "the build must measure it
+ * with an FFMA microbenchmark"): the roofline denominator of the SIMT sketches.  Runs on the
+ * current device on a private stream and synchronises; best of 5 timed launches of
+ * (SMs x 8) CTAs x 256 threads, each thread 16 independent FMA recurrences.
+ * mode 0: 3-register FFMA; 1: FFMA2 (fma.rn.f32x2, the form the SIMT sketches issue);
+ * 2: FFMA with immediate operands.  *tflops = 2 x FMAs / time; *ms (may be NULL) = the
+ * launch time.  TUNER_EINVAL for a bad mode or NULL tflops, TUNER_ECUDA without a device. */
+tuner_status tuner_probe_fp32_peak(int32_t mode, double* tflops, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

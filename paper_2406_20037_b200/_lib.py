@@ -99,6 +99,7 @@ SIGNATURES = {
     "tuner_destroy": (None, [C.c_void_p]),
     "tuner_last_error": (C.c_char_p, []),
     "tuner_global_launch_count": (C.c_int64, []),
+    "tuner_probe_fp32_peak": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 
 _LIB = None

@@ -99,6 +99,14 @@ def global_launch_count() -> int:
     return int(L.lib().tuner_global_launch_count())
 
 
+def probe_fp32_peak(mode: int = 1) -> Tuple[float, float]:
+    """FP32 pipe peak on the current device (tuner_probe_fp32_peak): (TFLOP/s, ms).
+    mode 0 = 3-register FFMA, 1 = FFMA2, 2 = immediate-operand FFMA."""
+    tf, ms = C.c_double(), C.c_double()
+    L.check(L.lib().tuner_probe_fp32_peak(mode, C.byref(tf), C.byref(ms)))
+    return tf.value, ms.value
+
+
 def _shape(op: str, shape: Dict, dtype: str) -> L.Shape:
     s = L.Shape()
     s.dtype = L.DTYPE[dtype]

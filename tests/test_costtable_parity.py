@@ -145,3 +145,11 @@ def test_sample_exhausts_gracefully():
     got = t.sample(100)
     assert len(got) == 6 and len({s.point for s in got}) == 6
     assert t.sample(5) == []
+
+
+def test_sampler_hand_trace_product():
+    # tests/test_oracle_pins_r2.py::test_sampler_hand_traced_with_rejected_draw through tuner_sample:
+    # draw 1 (1,(1,)) is invalid and rejected, draws 2-3 give (0,(1,)), (0,(0,)) (published outputs #1-#6)
+    t = Tuner("dense", {"m": 1, "n": 1, "k": 1}, spaces=[(0, [[10, 20]]), (1, [[1, 2, 3]])],
+              cost_table=[1.0, 2.0, 3.0, math.inf, 5.0], seed=0)
+    assert [s.point for s in t.sample(2)] == [(0, (1,)), (0, (0,))]

@@ -67,3 +67,12 @@ def test_single_layer_gets_the_budget_and_heavy_layer_gets_more():
     ot3 = oracle_tuners(ls3, 8)
     used = oschedule(ot3, [1.0, 1.0, 1.0], 300, pop=8, elite=4)
     assert used[0] > used[1] and used[0] > used[2]
+
+
+@pytest.mark.parametrize("c2,w2,expect", [(0.1, 1.0, [4, 4, 30]), (10.0, 1.0, [4, 4, 64]), (0.1, 100.0, [4, 4, 64])])
+def test_drop_rule_hand_derived_product(c2, w2, expect):
+    # the hand-derived drop cases of tests/test_oracle_pins_r2.py::test_drop_rule_hand_derived
+    # through tuner_schedule in cost-table mode
+    ts = [Tuner("dense", {"m": 1, "n": 1, "k": 1}, spaces=[(0, [list(range(n))])], cost_table=np.full(n, c),
+                seed=n) for n, c in ((4, 100.0), (4, 50.0), (64, c2))]
+    assert schedule(ts, [1.0, 1.0, w2], 90, increment=16, drop_frac=0.01, pop=16, elite=4) == expect

@@ -67,3 +67,14 @@ def test_significance_stops_earlier_than_strict_compare():
     r2 = stat.droplet((1, (0, 0)), 100)
     assert r2["trials_used"] <= r1["trials_used"]
     assert len(r2["traj"]) <= len(r1["traj"])
+
+
+@pytest.mark.parametrize("alpha,moves", [(0.0, True), (0.05, False), (0.1, False), (0.15, True)])
+def test_alpha_gate_spec_example_product(alpha, moves):
+    # SPEC S:228 ({1,2,3} vs {4,5,6}: p = 0.1; "tie when p >= alpha") through the C++ Droplet
+    cost = np.array([5.0, 2.0])
+    smp = np.array([[4.0, 5.0, 6.0], [1.0, 2.0, 3.0]])
+    t = Tuner("dense", {"m": 1, "n": 1, "k": 1}, spaces=[(0, [[0, 1]])], cost_table=cost, cost_samples=smp,
+              policy="plain", alpha=alpha)
+    rep = t.droplet((0, (0,)), 100)
+    assert rep["best"] == ((0, (1,)) if moves else (0, (0,))) and rep["converged"] and rep["trials_used"] == 2
