@@ -48,8 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--json-out", default=None)
-    ap.add_argument("--no-bf16-probe", action="store_true",
-                    help="skip the untimed tensor-core probe (DPAnsor on two compute-bound bf16 layers)")
+    ap.add_argument("--no-bf16-block", action="store_true",
+                    help="skip the timed tensor-core block (the same tuning job on two compute-bound bf16 layers)")
     return ap.parse_args()
 
 
@@ -62,36 +62,85 @@ def layers_for(name):
             "bert": (BERT, "bf16"), "bert1": (bert(batch=1), "bf16"), "config1": ([CONFIG1], "f32")}[name]
 
 
-def peaks():
+def peaks(measure_fp32=True):
+    """Roofline denominators: HBM GB/s and bf16 TFLOP/s from MEASURED_PEAKS.json (driver-written);
+    the FP32 pipe peak MEASURED here, on this GPU, by the library's FFMA2 microbenchmark
+    (tuner_probe_fp32_peak; committed runs: profiles/r2_fp32_peak.json)."""
     mp = {}
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     sm_mhz = float(mp.get("sm_max_mhz", 1965.0))
-    # FP32 FFMA peak from unit counts and clock (B200_PROFILING.md: 148 SMs; 128 FP32 lanes/SM, 2 flop/FFMA)
-    fp32_tflops = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-    return {"fp32_tflops": fp32_tflops, "sm_max_mhz": sm_mhz, "hbm_gbs": float(mp.get("hbm_gbs", 6650.0)),
-            "bf16_tflops": float(mp.get("bf16_tflops", 1590.0)),
+    derived = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # unit counts x clock (B200_PROFILING.md), for reference
+    fp32, src = derived, f"derived 148 SM x 128 lanes x 2 x {sm_mhz:.0f} MHz (probe unavailable)"
+    if measure_fp32:
+        try:
+            from paper_2406_20037_b200 import probe_fp32_peak
+            fp32 = max(probe_fp32_peak(1)[0] for _ in range(3))
+            src = "measured in this run: FFMA2 microbenchmark (tuner_probe_fp32_peak), best of 3 x 5 launches"
+        except Exception as e:  # noqa: BLE001
+            src += f"; probe failed: {e}"
+    return {"fp32_tflops": fp32, "fp32_source": src, "fp32_derived": derived, "sm_max_mhz": sm_mhz,
+            "hbm_gbs": float(mp.get("hbm_gbs", 6540.8)), "bf16_tflops": float(mp.get("bf16_tflops", 1608.9)),
             "source": "MEASURED_PEAKS.json" if mp else "B200_PROFILING.md fallback"}
 
 
-def traffic_evidence():
-    """DRAM traffic of a best r18.l1.3x3 schedule (cp.async sketch, split-K 8) from the committed
-    ncu --set full capture (profiles/r1_ncu_pipe5_r18l1.raw.csv) next to the layer's algorithmic bytes."""
-    import csv
-    path = os.path.join(ROOT, "profiles", "r1_ncu_pipe5_r18l1.raw.csv")
+def cpu_model():
     try:
-        rows = list(csv.reader(open(path)))
-        d = {h: (v, u) for h, u, v in zip(rows[0], rows[1], rows[2])}
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        by = sum(float(d[m][0].replace(",", "")) * scale.get(d[m][1], 1)
-                 for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def layer_min_bytes(L, in_bytes):
+    """SURVEY §8(d).4 algorithmic bytes of one execution: sizeof(in)(|X| + |W|) + 4|Y|."""
+    from synth.workloads import out_hw
+    if L["op"] == "conv2d":
+        P, Q = out_hw(L)
+        x = L["N"] * L["H"] * L["W"] * L["C"]
+        w = L["K"] * L["R"] * L["S"] * L["C"]
+        y = L["N"] * P * Q * L["K"]
+    else:
+        b = L.get("b", 1)
+        x, w, y = b * L["m"] * L["k"], b * L["n"] * L["k"], b * L["m"] * L["n"]
+    return in_bytes * (x + w) + 4 * y
+
+
+def simt_ctas(L, sketch, vals):
+    """Grid size (CTAs) of a SIMT implicit-GEMM / GEMM schedule (sketches 0, 1, 4, 7, 8): one CTA
+    per BM x BN output tile per k split; None for the other sketches."""
+    from synth.workloads import out_hw
+    if sketch not in (0, 1, 4, 7, 8):
+        return None
+    if L["op"] == "conv2d":
+        P, Q = out_hw(L)
+        M, N, B = L["N"] * P * Q, L["K"], 1
+    else:
+        M, N, B = L["m"], L["n"], L.get("b", 1)
+    return -(-M // vals[0]) * -(-N // vals[1]) * vals[7] * B
+
+
+def traffic_evidence(tuned):
+    """roofline.traffic: dram__bytes_read.sum + dram__bytes_write.sum per launch of the timed layers'
+    best schedules, from the committed ncu --set full captures (profiles/traffic_r2.json, written by
+    tools/capture_traffic.py from a bench run's best schedules; ncu flushes the caches before each
+    replay, so these are cold-cache bytes).  Mean over the timed layers that have a capture."""
+    path = os.path.join(ROOT, "profiles", "traffic_r2.json")
+    try:
+        cap = json.load(open(path))
     except Exception:
         return None
-    algo = 4 * (56 * 56 * 64 + 64 * 9 * 64 + 56 * 56 * 64)  # X + W + Y, fp32
-    return {"capture": "profiles/r1_ncu_pipe5_r18l1.raw.csv", "layer": "r18.l1.3x3", "dram_bytes": by,
-            "algorithmic_bytes": algo, "ratio": by / algo}
+    got = [cap[r["layer"]] for r in tuned if r["layer"] in cap]
+    if not got:
+        return None
+    same = sum(1 for r in tuned if r["layer"] in cap and cap[r["layer"]].get("schedule") == r.get("dp_best"))
+    return {"dram_bytes_per_launch": sum(g["dram_bytes"] for g in got) / len(got),
+            "source": f"profiles/traffic_r2.json: {len(got)}/{len(tuned)} timed layers captured "
+                      f"({same} with this run's exact best schedule)"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -223,7 +272,7 @@ def main():
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r, n, el, cores, names = oracle_rate(layers[:11], 12.0)
-        cpu_baseline = {"value": r, "unit": "candidates/s", "cores": cores, "kind": "oracle",
+        cpu_baseline = {"value": r, "unit": "candidates/s", "cores": cores, "kind": "oracle", "cpu": cpu_model(),
                         "sample": f"{n} direct-loop fp64 evaluations over {len(set(names))} {args.workload} layers "
                                   f"({el:.1f} s; one evaluation = one candidate measurement)"}
 
@@ -257,16 +306,18 @@ def main():
             return [(sk, sketch_space(sk)) for sk in sks]
         return None
 
-    def tune_layer(li, seed, e2e=False, pinned=None):
-        L = layers[li]
-        xd, wd, y = bufs[li][:3]
+    def tune_layer(li, seed, e2e=False, pinned=None, lay=None, bf=None, dt=None, spaces=None):
+        L = layers[li] if lay is None else lay
+        xd, wd, y = (bufs[li][:3] if bf is None else bf)
+        dt = dtype if dt is None else dt
+        sp = spaces_of(L) if spaces is None else spaces
         if e2e:  # host -> device copy of the step's inputs inside the timed region
             xd.copy_(pinned[0], non_blocking=True)
             wd.copy_(pinned[1], non_blocking=True)
         rec = {"layer": L["name"], "gflop": layer_flops(L) / 1e9}
-        # DPAnsor: sample N, best-of-N, Droplet to convergence (<= 100 trials)
+        # DPAnsor: explore N, best-of-N, Droplet to convergence (<= 100 trials)
         t0 = time.perf_counter()
-        tu = Tuner(L["op"], shape_of(L), dtype=dtype, spaces=spaces_of(L), x=xd, w=wd, y=y, seed=seed, group=group,
+        tu = Tuner(L["op"], shape_of(L), dtype=dt, spaces=sp, x=xd, w=wd, y=y, seed=seed, group=group,
                    stream=stream, early_cut=args.early_cut)
         smp = tu.evolve(args.n_sample) if args.explore == "evolve" else tu.sample(args.n_sample)
         if not smp:  # no compiled sketch covers this layer (e.g. bf16 TMA needs C % 8 == 0)
@@ -277,19 +328,25 @@ def main():
         rep = tu.droplet(b.point, args.droplet_budget)
         t1 = time.perf_counter()
         st = tu.stats()
-        rec.update(dp_best_ns=rep["best_cost"], dp_best=tu.values(rep["best"]), sample_best_ns=b.cost_ns,
-                   droplet_trials=rep["trials_used"], droplet_rounds=rep["rounds"], converged=rep["converged"],
-                   dp_wall_s=t1 - t0, dp_candidates=st["candidates"], launches=st["kernel_launches"],
-                   collectives=st["collectives"], wrong=sum(s.status != "ok" for s in tu.history()))
+        rec.update(dp_best_ns=rep["best_cost"], dp_point=rep["best"], sketch=rep["best"][0],
+                   dp_best=tu.values(rep["best"]),
+                   sample_best_ns=b.cost_ns, droplet_trials=rep["trials_used"], droplet_rounds=rep["rounds"],
+                   converged=rep["converged"], dp_wall_s=t1 - t0, dp_candidates=st["candidates"],
+                   launches=st["kernel_launches"], collectives=st["collectives"],
+                   wrong=sum(s.status != "ok" for s in tu.history()))
+        cut, precise = st["early_cut"], st["precise"]
         # the 10,000-trial random baseline on the same harness (fresh history, other seed)
-        bl = Tuner(L["op"], shape_of(L), dtype=dtype, spaces=spaces_of(L), x=xd, w=wd, y=y, seed=seed + 7919,
+        bl = Tuner(L["op"], shape_of(L), dtype=dt, spaces=sp, x=xd, w=wd, y=y, seed=seed + 7919,
                    group=group, stream=stream, early_cut=args.early_cut)
         bl.sample(args.baseline) if args.baseline > 0 else None
         t2 = time.perf_counter()
         bst = bl.stats()
         bb = bl.best() if bst["candidates"] else None
-        rec.update(bl_best_ns=bb.cost_ns if bb else math.inf, bl_wall_s=t2 - t1, bl_candidates=bst["candidates"],
-                   launches=rec["launches"] + bst["kernel_launches"], collectives=rec["collectives"] + bst["collectives"])
+        rec.update(bl_best_ns=bb.cost_ns if bb else math.inf, bl_point=bb.point if bb else None,
+                   bl_best=bl.values(bb.point) if bb else None, bl_wall_s=t2 - t1, bl_candidates=bst["candidates"],
+                   launches=rec["launches"] + bst["kernel_launches"], collectives=rec["collectives"] + bst["collectives"],
+                   early_cut=cut + bst["early_cut"], precise=precise + bst["precise"],
+                   calibrations=st["calibrations"] + bst["calibrations"])
         if e2e:  # device -> host read of the step's result: the best schedule's output
             tu.run(rep["best"], xd, wd, y, stream=stream)
             rec["y_host_sum"] = float(y.to("cpu", non_blocking=False).double().sum())
@@ -297,6 +354,29 @@ def main():
         tu.close()
         rec["candidates"] = rec["dp_candidates"] + rec["bl_candidates"]
         return rec
+
+    def retime(rec, li=None, lay=None, bf=None, dt=None, spaces=None):
+        """Outside the timed region: the DPAnsor best and the 10k best re-timed back to back by a
+        fresh tuner in one batch (same window, same GPU), R = 10 repeats each; the
+        reported quality ratio uses these costs, with the two-sided Wilcoxon rank-sum p of the
+        repeat timings (significance at p < 0.01)."""
+        from paper_2406_20037_b200 import rank_sum_p
+        if rec.get("skipped") or rec.get("bl_point") is None:
+            return
+        L = layers[li] if lay is None else lay
+        xd, wd, y = (bufs[li][:3] if bf is None else bf)
+        dt = dtype if dt is None else dt
+        sp = spaces_of(L) if spaces is None else spaces
+        arb = Tuner(L["op"], shape_of(L), dtype=dt, spaces=sp, x=xd, w=wd, y=y, seed=1, stream=stream, repeats=10)
+        pts = [rec["dp_point"], rec["bl_point"]]
+        if pts[0] == pts[1]:
+            r = arb.measure(pts[:1])[0]
+            rec.update(rt_dp_ns=r.cost_ns, rt_bl_ns=r.cost_ns, rt_p=1.0)
+        else:
+            rs = arb.measure(pts)
+            ta, tb = arb.timings(pts[0]), arb.timings(pts[1])
+            rec.update(rt_dp_ns=rs[0].cost_ns, rt_bl_ns=rs[1].cost_ns, rt_p=rank_sum_p(ta, tb))
+        arb.close()
 
     def barrier():
         if world > 1:
@@ -325,6 +405,9 @@ def main():
         recs.append(rec)
     launches = global_launch_count() - l0
     clocks = sampler.stop()
+    if world == 1:
+        for s, rec in enumerate(recs):
+            retime(rec, s % len(layers))
 
     # max over ranks
     tot_ms = sum(step_ms)
@@ -338,26 +421,41 @@ def main():
     cands = sum(r["candidates"] for r in recs)
     value = cands / (tot_ms / 1e3)
 
-    # tensor-core probe (outside the timed region): 300 samples + Droplet on two compute-bound
-    # bf16 layers of configs[2]/[3], reported against the measured bf16 peak
-    probe = None
-    if dtype == "f32" and not args.no_bf16_probe and world == 1:
+    # configs[2]/[3] tensor-core block: the same tuning job (300 + Droplet vs 10k random) on two
+    # compute-bound bf16 layers (VGG-16 512->512 @28 b16 conv, BERT-base FFN1 b16 dense), each
+    # bracketed by CUDA events like a step, against the measured bf16 peak
+    bf16 = None
+    if dtype == "f32" and not args.no_bf16_block and world == 1:
         from synth import BERT, VGG16
-        probe = {"unit": "TFLOP/s", "peak": pk["bf16_tflops"], "bound": "tensor", "layers": []}
-        for L in (VGG16[7], BERT[3]):
+        bl16 = []
+        ev_ms = 0.0
+        for L in (VGG16[7], BERT[2]):
             x, w = layer_tensors(L, 0x5EED)
-            xd = torch.from_numpy(x).to(dev).to(torch.bfloat16)
-            wd = torch.from_numpy(w).to(dev).to(torch.bfloat16)
-            y = torch.empty(out_shape(L), device=dev)
-            tu = Tuner(L["op"], shape_of(L), dtype="bf16", x=xd, w=wd, y=y, seed=0, stream=stream,
-                       early_cut=args.early_cut)
-            tu.sample(args.n_sample)
-            rep = tu.droplet(tu.best().point, args.droplet_budget)
-            tf = layer_flops(L) / rep["best_cost"] / 1e3
-            probe["layers"].append({"layer": L["name"], "best": tu.values(rep["best"]),
-                                    "best_ns": rep["best_cost"], "achieved": tf, "frac": tf / pk["bf16_tflops"]})
-            tu.close()
-            del xd, wd, y
+            bb16 = (torch.from_numpy(x).to(dev).to(torch.bfloat16), torch.from_numpy(w).to(dev).to(torch.bfloat16),
+                    torch.empty(out_shape(L), device=dev))
+            tune_layer(0, seed=900, lay=L, bf=bb16, dt="bf16", spaces=None)  # warm-up (untimed)
+            flush.zero_()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = tune_layer(0, seed=0, lay=L, bf=bb16, dt="bf16", spaces=None)
+            e1.record(stream)
+            barrier()
+            ev_ms += e0.elapsed_time(e1)
+            retime(r, lay=L, bf=bb16, dt="bf16", spaces=None)
+            bl16.append(r)
+            del bb16
+        fl = sum(r["gflop"] * 1e9 for r in bl16)
+        ach = fl / (sum(r["dp_best_ns"] for r in bl16) * 1e-9) / 1e12
+        bf16 = {"layers": [{"layer": r["layer"], "best": r["dp_best"], "best_ns": round(r["dp_best_ns"], 1),
+                            "tflops": round(r["gflop"] / r["dp_best_ns"] * 1e6, 1),
+                            "frac_peak": round(r["gflop"] / r["dp_best_ns"] * 1e6 / pk["bf16_tflops"], 3),
+                            "dp_over_10k": round(r["rt_dp_ns"] / r["rt_bl_ns"], 3), "p": r["rt_p"],
+                            "candidates": r["candidates"], "bl_valid_space_exhausted": r["bl_candidates"] < args.baseline}
+                           for r in bl16],
+                "achieved": ach, "peak": pk["bf16_tflops"], "frac": ach / pk["bf16_tflops"], "unit": "TFLOP/s",
+                "candidates_per_s": sum(r["candidates"] for r in bl16) / (ev_ms / 1e3), "timed_ms": ev_ms}
 
     # e2e: host buffers through the public API, H2D + D2H inside the timed region
     e2e = None
@@ -382,48 +480,76 @@ def main():
         e2e = {"value": e_c / el, "unit": "candidates/s", "h2d_bytes_per_step": h2d // args.steps,
                "d2h_bytes_per_step": d2h // args.steps}
 
-    # roofline of the dominant kernel = the best schedule found (FP32 pipe, CUDA-event median per launch)
+    # roofline of the dominant kernel = the best schedule found per timed layer
+    # (sum F / sum per-launch CUDA-event time measured by the harness inside the timed region)
     tuned = [r for r in recs if not r.get("skipped")]
     fl = sum(r["gflop"] * 1e9 for r in tuned)
     dp_ns = sum(r["dp_best_ns"] for r in tuned)
     achieved = fl / (dp_ns * 1e-9) / 1e12
+    in_bytes = 4 if dtype == "f32" else 2
     if dtype == "f32":
         peak = pk["fp32_tflops"]
-        roofline = {"bound": "alu", "peak_source": f"148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz "
-                                                   "(derived from B200_PROFILING.md unit counts; no measured FP32 peak)"}
+        roofline = {"bound": "alu", "peak_source": pk["fp32_source"]}
     else:
         peak = pk["bf16_tflops"]
         roofline = {"bound": "tensor", "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst) = {peak}"}
-    roofline.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                     "kernel": "best 300+Droplet schedule per timed layer; sum F / sum per-launch CUDA-event time (precise tier, R-M4)"})
-    ev = traffic_evidence() if dtype == "f32" else None
-    if ev:
-        roofline["traffic_evidence"] = ev
+    # per layer: TFLOP/s / peak and / min(peak, AI x BW), CTAs per SM
+    per = []
+    for r in tuned:
+        L = next(x for x in layers if x["name"] == r["layer"])
+        byts = layer_min_bytes(L, in_bytes)
+        tf = r["gflop"] / r["dp_best_ns"] * 1e6
+        att = min(peak, r["gflop"] * 1e9 / byts * pk["hbm_gbs"] / 1e3)
+        ctas = simt_ctas(L, r["dp_point"][0], r["dp_best"])
+        per.append({"layer": r["layer"], "ns": round(r["dp_best_ns"]), "tf": round(tf, 2),
+                    "f_peak": round(tf / peak, 3), "f_roof": round(tf / att, 3),
+                    "cta_sm": round(ctas / 148, 2) if ctas else None, "sk": r["dp_point"][0],
+                    "q": round(r["rt_dp_ns"] / r["rt_bl_ns"], 3) if "rt_dp_ns" in r else None,
+                    "p": (float(f"{r['rt_p']:.2g}") if "rt_p" in r else None)})
+    alg_bytes = sum(layer_min_bytes(next(x for x in layers if x["name"] == r["layer"]), in_bytes) for r in tuned)
+    tr = traffic_evidence(tuned) if dtype == "f32" else None
+    roofline.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": tr["dram_bytes_per_launch"] if tr else None,
+                     "algorithmic_bytes_per_launch": alg_bytes / max(1, len(tuned)),
+                     "kernel": "best 300+Droplet schedule per timed layer; sum F / sum per-launch CUDA-event time"})
+    if tr:
+        roofline["traffic_source"] = tr["source"]
     dp_wall = sum(r["dp_wall_s"] for r in tuned)
     bl_wall = sum(r["bl_wall_s"] for r in tuned)
-    quality = [r["dp_best_ns"] / r["bl_best_ns"] for r in tuned if r["bl_best_ns"] < math.inf]
+    qual = [r["rt_dp_ns"] / r["rt_bl_ns"] for r in tuned if r.get("rt_bl_ns")]
+    if not qual:
+        qual = [r["dp_best_ns"] / r["bl_best_ns"] for r in tuned if r["bl_best_ns"] < math.inf]
+    sig_slower = sum(1 for r in tuned if r.get("rt_p", 1.0) < 0.01 and r["rt_dp_ns"] > r["rt_bl_ns"])
+    n_cut = sum(r.get("early_cut", 0) for r in tuned)
+    n_prec = sum(r.get("precise", 0) for r in tuned)
     line = {
         "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": dtype, "data": "synthetic",
         "config": {"workload": f"{args.workload} layers ({dtype}): {args.n_sample} samples + Droplet "
                                f"(<= {args.droplet_budget}) vs {args.baseline}-trial random baseline, one layer per step",
-                   "layers": [r["layer"] for r in recs], "l2": "flushed between steps; candidate timings hot-L2 "
-                   "(back-to-back launches)", "early_cut": args.early_cut, "parallelism": f"candidates sharded x{world}"},
+                   "l2": "flushed between steps (256 MB write); candidate timings hot-L2 (back-to-back launches)",
+                   "early_cut": args.early_cut, "parallelism": f"candidates sharded x{world}"},
+        "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu_baseline,
+        "tuning_wall_s": {"dpansor": round(dp_wall, 3), "baseline_10k": round(bl_wall, 3),
+                          "speedup": round(bl_wall / dp_wall, 2) if dp_wall > 0 else None},
+        "early_cut_frac": round(n_cut / max(1, cands), 4), "precise_frac": round(n_prec / max(1, cands), 4),
+        "bf16": bf16,
+        "per_layer": per,
+        "quality_dp_over_10k": {"retimed": "rt_dp_ns" in (tuned[0] if tuned else {}),
+                                "geomean": math.exp(sum(math.log(q) for q in qual) / len(qual)) if qual else None,
+                                "max": max(qual) if qual else None, "within_5pct": sum(q <= 1.05 for q in qual),
+                                "layers": len(qual), "dp_significantly_slower_p01": sig_slower},
         "best_schedule_tflops": achieved, "best_schedule_pct_peak": 100 * achieved / peak,
-        "tuning_wall_s": {"dpansor": dp_wall, "baseline_10k": bl_wall,
-                          "speedup": bl_wall / dp_wall if dp_wall > 0 else None},
-        "quality_dp_over_10k": {"geomean": math.exp(sum(math.log(q) for q in quality) / len(quality)) if quality else None,
-                                "max": max(quality) if quality else None,
-                                "within_5pct": sum(q <= 1.05 for q in quality), "layers": len(quality)},
-        "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
-        "cpu_baseline": cpu_baseline, "bf16_probe": probe, "per_layer": recs,
+        "roofline": roofline,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
         if args.json_out:
+            full = dict(line)
+            full["per_layer_full"] = [{k: v for k, v in r.items() if k not in ("dp_point", "bl_point")} for r in recs]
             with open(args.json_out, "w") as f:
-                json.dump(line, f, indent=1)
+                json.dump(full, f, indent=1, default=str)
     if world > 1:
         dist.destroy_process_group()
 

@@ -175,6 +175,12 @@ typedef struct {
     const float* y_ref;
     const float* y_absref; /* sum |x||w| per output, device fp32 */
     void* stream;          /* cudaStream_t (e.g. a torch stream); NULL = default */
+    /* optional append-only JSONL trial log: every measured
+     * candidate is appended as one line keyed by the problem (op, shape, dtype); at create,
+     * the lines of an existing log with this tuner's key and sketches are replayed into the
+     * history (no re-measurement: a killed tuning job resumes where it stopped).  NULL = off.
+     * Rank 0 writes; every rank replays.  A malformed line -> TUNER_EINVAL at create. */
+    const char* trial_log;
 } tuner_opts;
 
 typedef struct {
@@ -277,7 +283,10 @@ tuner_status tuner_history(const tuner_t* t, tuner_result* out, int64_t cap, int
 
 /* Run candidate `cfg` once on caller buffers, asynchronously on `stream`
  * (NULL = the tuner's stream).  Split-K schedules zero y first (part of the
- * schedule).  ERANGE if cfg is statically invalid; ESTATE in cost-table mode. */
+ * schedule).  ERANGE if cfg is statically invalid; ESTATE in cost-table mode.
+ * Stream-K schedules (tcgen05 SCHED >= 1) use a workspace owned by the handle,
+ * allocated at the first such launch: that launch must not be inside a stream
+ * capture (ESTATE), and such launches of one handle must be ordered (one stream). */
 tuner_status kernel_run(const tuner_t* t, const tuner_point* cfg, const tuner_buffers* buf,
                         void* stream);
 
@@ -287,13 +296,22 @@ tuner_status tuner_reference(const tuner_t* t, const tuner_buffers* buf, float* 
                              float* y_absref, void* stream);
 
 /* Counters since create: candidate kernel launches (incl. graph nodes),
- * measured candidates, collectives issued, host wall ns inside measurement. */
+ * measured candidates, collectives issued, host wall ns inside measurement; and the
+ * measurement tiers (measured mode, this rank): early_cut = candidates ranked by their
+ * verify run alone (R-M3), light = candidates timed with 3 repeats instead of R,
+ * precise = candidates re-timed over the long windows of R-M4, calibrations = cross-rank
+ * batch winners re-timed on rank 0 (world > 1). */
 typedef struct {
     int64_t kernel_launches;
     int64_t candidates;
     int64_t collectives;
     int64_t batches;
     double measure_wall_ns;
+    int64_t early_cut;
+    int64_t light;
+    int64_t precise;
+    int64_t calibrations;
+    int64_t replayed; /* history entries restored from opts.trial_log at create */
 } tuner_stats;
 tuner_status tuner_get_stats(const tuner_t* t, tuner_stats* out);
 
@@ -305,6 +323,13 @@ const char* tuner_last_error(void);
 
 /* Total candidate-kernel launches by this process (all handles). */
 int64_t tuner_global_launch_count(void);
+
+/* The significance test of the paper's methodology ("the p-value (produced via the
+ * non-parametric Wilcoxon rank-sum test)"; reading R-W1): two-sided exact rank-sum
+ * test on midranks of the samples a[n1] and b[n2] (e.g. two candidates' repeat timings from
+ * tuner_timings) -> *p in (0, 1]; 1 when either side is empty.  EINVAL for NULL pointers or
+ * more than 16 samples per side.  The same routine gates Droplet's moves when alpha > 0. */
+tuner_status tuner_rank_sum_p(const float* a, int32_t n1, const float* b, int32_t n2, double* p);
 
 /* FP32 pipe peak microbenchmark (BASELINE.md §2 "the build must measure it
  * with an FFMA microbenchmark"): the roofline denominator of the SIMT sketches.  Runs on the

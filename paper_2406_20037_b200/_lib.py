@@ -54,7 +54,8 @@ class Opts(C.Structure):
                 ("cost_samples", C.POINTER(C.c_double)), ("cost_nsamp", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("allgather", ALLGATHER_FN), ("allgather_ctx", C.c_void_p), ("x", C.c_void_p), ("w", C.c_void_p),
-                ("y", C.c_void_p), ("y_ref", C.c_void_p), ("y_absref", C.c_void_p), ("stream", C.c_void_p)]
+                ("y", C.c_void_p), ("y_ref", C.c_void_p), ("y_absref", C.c_void_p), ("stream", C.c_void_p),
+                ("trial_log", C.c_char_p)]
 
 
 class DropletReport(C.Structure):
@@ -68,7 +69,9 @@ class Buffers(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("candidates", C.c_int64), ("collectives", C.c_int64),
-                ("batches", C.c_int64), ("measure_wall_ns", C.c_double)]
+                ("batches", C.c_int64), ("measure_wall_ns", C.c_double), ("early_cut", C.c_int64),
+                ("light", C.c_int64), ("precise", C.c_int64), ("calibrations", C.c_int64),
+                ("replayed", C.c_int64)]
 
 
 # name -> (restype, argtypes); every function declared in include/tuner.h
@@ -99,6 +102,8 @@ SIGNATURES = {
     "tuner_destroy": (None, [C.c_void_p]),
     "tuner_last_error": (C.c_char_p, []),
     "tuner_global_launch_count": (C.c_int64, []),
+    "tuner_rank_sum_p": (C.c_int, [C.POINTER(C.c_float), C.c_int32, C.POINTER(C.c_float), C.c_int32,
+                                   C.POINTER(C.c_double)]),
     "tuner_probe_fp32_peak": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 

@@ -22,7 +22,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <thread>
 #include <cstring>
 #include <mutex>
 #include <unordered_set>
@@ -58,6 +60,83 @@ static tuner_status cuda_fail(cudaError_t e, const char* what) {
         cudaError_t e_ = (call);                            \
         if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
     } while (0)
+
+// The handle's stream-K workspace: allocated on the first launch
+// of a SCHED >= 1 schedule, never inside a stream capture (cudaMalloc / cudaMemset are not
+// capturable), sized for every co-resident CTA (4 slots per SM covers any persistent grid).
+static tuner_status ensure_streamk(Tuner* t, cudaStream_t st) {
+    if (t->sk.flags) return TUNER_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CU(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+        return fail(TUNER_ESTATE, "a stream-K schedule's first launch on this handle cannot be captured "
+                                  "(its workspace is allocated then): run it once outside the capture");
+    int dev = 0, nsm = 148;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int slots = 4 * nsm;
+    unsigned* f = nullptr;
+    float* w = nullptr;
+    CU(cudaMalloc(&f, (size_t)slots * sizeof(unsigned)));
+    cudaError_t e = cudaMalloc(&w, (size_t)slots * 128 * 256 * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemsetAsync(f, 0, (size_t)slots * sizeof(unsigned), st);
+    if (e != cudaSuccess) {
+        cudaFree(f);
+        if (w) cudaFree(w);
+        return cuda_fail(e, "stream-K workspace");
+    }
+    t->sk.flags = f;
+    t->sk.ws = w;
+    t->sk.slots = slots;
+    t->sk.dev = dev;
+    return TUNER_OK;
+}
+
+Tuner::~Tuner() {
+    if (trial_log) std::fclose(trial_log);
+    measurer.reset();  // the GPU measurer synchronises its device first
+    if (sk.flags) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(sk.dev);
+        cudaDeviceSynchronize();  // kernel_run launches on caller streams may still use it
+        cudaFree(sk.flags);
+        cudaFree(sk.ws);
+        cudaSetDevice(cur);
+    }
+}
+
+// Watchdog: wait for a phase by polling its ordered progress events (one per
+// candidate run / timing window).  If none completes for `stall_ms`, a candidate kernel hangs --
+// e.g. a spin-wait whose partner CTA never became resident -- and the call returns TUNER_ECUDA
+// (the handle is then dead) instead of blocking the caller forever.  Every window is bounded by
+// max(20 us, one launch) < timeout_ms, so stall_ms = max(5 s, 4 x timeout_ms) never fires on a
+// live device.
+static tuner_status wait_progress(const std::vector<cudaEvent_t>& evs, double stall_ms) {
+    using clk = std::chrono::steady_clock;
+    auto last = clk::now();
+    size_t i = 0;
+    unsigned polls = 0;
+    while (i < evs.size()) {
+        const cudaError_t q = cudaEventQuery(evs[i]);
+        if (q == cudaSuccess) {
+            ++i;
+            last = clk::now();
+            polls = 0;
+            continue;
+        }
+        if (q != cudaErrorNotReady) return cuda_fail(q, "cudaEventQuery");
+        if (++polls > 256) {  // spin briefly (phases end within microseconds), then back off
+            if (std::chrono::duration<double, std::milli>(clk::now() - last).count() > stall_ms)
+                return fail(TUNER_ECUDA, "watchdog: no candidate finished for " + std::to_string((long)stall_ms) +
+                                             " ms (a kernel hangs; the device is left busy)");
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        } else {
+            std::this_thread::yield();
+        }
+    }
+    return TUNER_OK;
+}
 
 // launcher + runtime knobs of a point
 struct RuntimeKnobs {
@@ -224,50 +303,101 @@ struct GpuMeasurer : Measurer {
         return resolve(t, p, rk) != nullptr;
     }
 
-    tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out, double incumbent) override {
-        const size_t n = pts.size();
-        out.assign(n, Result{});
-        if (n == 0) return TUNER_OK;
+    // ---- one rank's share of a batch, in three phases with a host sync each
+    struct Batch {
+        size_t n = 0;
+        std::vector<LaunchFn> fn;
+        std::vector<RuntimeKnobs> rk;
+        std::vector<char> launched, cut, precise;
+        std::vector<double> tver;
+        std::vector<int> reps, warm, number, nlong;
+        std::vector<cudaGraphExec_t> execs;
+        size_t EB = 0, tb = 0;
+        double stall_ms = 5000.0;
+        std::vector<cudaEvent_t> prog;  // progress events of a phase, in stream order (watchdog)
+        LaunchCtx ctx{};
+    };
+
+    void set_knobs(Batch& b, size_t j) {
+        b.ctx.split = b.rk[j].split;
+        b.ctx.vec = b.rk[j].vec;
+        b.ctx.stages = b.rk[j].stages;
+        b.ctx.sched = b.rk[j].sched;
+        for (int d = 0; d < 3; ++d) b.ctx.dims[d] = b.rk[j].dims[d];
+        b.ctx.raster = b.rk[j].raster;
+    }
+
+    // nwin back-to-back windows of `num` launches of candidate j, bracketed by events
+    // ev[base..base+nwin]: a graph of G <= 8 launches replayed L times per window (few nodes to
+    // capture and instantiate on the host, back-to-back launches on the device); used = G * L
+    tuner_status time_windows(Batch& b, size_t j, int num, int nwin, size_t base, int& used) {
+        auto& ev = event_pool(dev);
+        const int G = std::min(num, kMaxGraphNodes);
+        const int L = (num + G - 1) / G;
+        used = G * L;
+        LaunchCtx cc = b.ctx;
+        cc.stream = cap;
+        set_capturing(true);
+        cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+        for (int i = 0; i < G && e == cudaSuccess; ++i) e = b.fn[j](cc);
+        cudaGraph_t g = nullptr;
+        cudaError_t e2 = cudaStreamEndCapture(cap, &g);
+        set_capturing(false);
+        if (e != cudaSuccess) return cuda_fail(e, "graph capture");
+        if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamEndCapture");
+        e = exec_for(g, b.execs[j]);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+        CU(cudaEventRecord(ev[base], st));
+        for (int r = 0; r < nwin; ++r) {
+            for (int l = 0; l < L; ++l) CU(cudaGraphLaunch(b.execs[j], st));
+            count_launches(used);
+            CU(cudaEventRecord(ev[base + r + 1], st));
+            b.prog.push_back(ev[base + r + 1]);
+        }
+        return TUNER_OK;
+    }
+
+    // phase 1: verification run (also the first, untimed-for-cost launch)
+    tuner_status phase_verify(const std::vector<Pt>& pts, Batch& b, std::vector<Result>& out) {
+        const size_t n = b.n;
         CU(cudaSetDevice(dev));
-        const int R = t->opts.repeats, W = t->opts.warmup;
-        const size_t EB = (size_t)R + 1 + kPreciseWindows;  // timing events per candidate
-        tuner_status s = ensure_events(dev, 2 * n + n * EB);
+        const int R = t->opts.repeats;
+        b.EB = (size_t)R + 1 + kPreciseWindows;  // timing events per candidate
+        b.tb = 2 * n;                            // timing events start here
+        tuner_status s = ensure_events(dev, 2 * n + n * b.EB);
         if (s != TUNER_OK) return s;
         auto& ev = event_pool(dev);
         if (err_cap < n) {
             if (d_err) cudaFree(d_err);
             if (h_err) cudaFreeHost(h_err);
+            d_err = nullptr;
+            h_err = nullptr;
+            err_cap = 0;
             CU(cudaMalloc(&d_err, n * sizeof(unsigned)));
             CU(cudaMallocHost(&h_err, n * sizeof(unsigned)));
             err_cap = n;
         }
-        std::vector<LaunchFn> fn(n);
-        std::vector<RuntimeKnobs> rk(n);
-        std::vector<char> launched(n, 0);
-        for (size_t j = 0; j < n; ++j) fn[j] = resolve(t, pts[j], rk[j]);
+        bool need_sk = false;
+        for (size_t j = 0; j < n; ++j) {
+            b.fn[j] = resolve(t, pts[j], b.rk[j]);
+            need_sk |= b.rk[j].sched >= 1;
+        }
+        if (need_sk && (s = ensure_streamk(t, st)) != TUNER_OK) return s;
         const size_t ybytes = (size_t)t->info.y_elems * sizeof(float);
-        LaunchCtx ctx{&t->info, t->opts.x, t->opts.w, t->opts.y, 1, 1, 1, 0, st, nsm};
-        auto set_knobs = [&](size_t j) {
-            ctx.split = rk[j].split;
-            ctx.vec = rk[j].vec;
-            ctx.stages = rk[j].stages;
-            ctx.sched = rk[j].sched;
-            for (int d = 0; d < 3; ++d) ctx.dims[d] = rk[j].dims[d];
-            ctx.raster = rk[j].raster;
-        };
-
-        // ---- phase 1: verification run (also the first, untimed-for-cost launch)
+        b.ctx = LaunchCtx{&t->info, t->opts.x, t->opts.w, t->opts.y, 1, 1, 1, 0, st, nsm};
+        b.ctx.sk = &t->sk;
         CU(cudaMemsetAsync(d_err, 0, n * sizeof(unsigned), st));
         for (size_t j = 0; j < n; ++j) {
-            set_knobs(j);
+            set_knobs(b, j);
             // one untimed launch the first time a launcher runs: module loading never
             // inflates t_verify (and so never causes a false early cut)
-            cudaError_t e = fn[j] ? cudaSuccess : cudaErrorInvalidDeviceFunction;
-            if (e == cudaSuccess && first_launch(dev, fn[j])) e = fn[j](ctx);
+            cudaError_t e = b.fn[j] ? cudaSuccess : cudaErrorInvalidDeviceFunction;
+            if (e == cudaSuccess && first_launch(dev, b.fn[j])) e = b.fn[j](b.ctx);
             if (e == cudaSuccess) {
                 if (t->opts.verify) CU(cudaMemsetAsync(t->opts.y, 0xFF, ybytes, st));
                 CU(cudaEventRecord(ev[2 * j], st));
-                e = fn[j](ctx);
+                e = b.fn[j](b.ctx);
                 CU(cudaEventRecord(ev[2 * j + 1], st));
             }
             if (e != cudaSuccess) {
@@ -275,92 +405,51 @@ struct GpuMeasurer : Measurer {
                 out[j].status = TUNER_S_LAUNCH_FAIL;
                 continue;
             }
-            launched[j] = 1;
+            b.launched[j] = 1;
+            b.prog.push_back(ev[2 * j + 1]);
             if (t->opts.verify)
                 CU(launch_verify((const float*)t->opts.y, ref, absref, t->info.y_elems, d_err + j, nsm, st));
         }
         CU(cudaMemcpyAsync(h_err, d_err, n * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        if ((s = wait_progress(b.prog, b.stall_ms)) != TUNER_OK) return s;
         CU(cudaStreamSynchronize(st));
-        std::vector<double> tver(n, 0.0);
         for (size_t j = 0; j < n; ++j) {
-            if (!launched[j]) continue;
+            if (!b.launched[j]) continue;
             float ms = 0.f;
             CU(cudaEventElapsedTime(&ms, ev[2 * j], ev[2 * j + 1]));
-            tver[j] = ms * 1e6;  // ns
+            b.tver[j] = ms * 1e6;  // ns
             float err;
             std::memcpy(&err, &h_err[j], sizeof(float));
             out[j].max_err = t->opts.verify ? (double)err : 0.0;
             if (t->opts.verify && !(err <= tol)) out[j].status = TUNER_S_WRONG;
             else if (ms > t->opts.timeout_ms) out[j].status = TUNER_S_TIMEOUT;
         }
+        return TUNER_OK;
+    }
 
-        // early cut (SURVEY d.5): rank hopeless candidates by their verify run
-        // and time clearly non-competitive ones (> 1.5x) with 3 repeats instead of R
-        std::vector<char> cut(n, 0);
-        std::vector<int> reps(n, R), warm(n, W);
-        (void)incumbent;
-        if (t->opts.early_cut > 0.0) {
-            double ref_ns = best_tver;
-            for (size_t j = 0; j < n; ++j)
-                if (out[j].status == TUNER_S_OK) ref_ns = std::min(ref_ns, tver[j]);
-            best_tver = ref_ns;
-            for (size_t j = 0; j < n; ++j) {
-                if (out[j].status != TUNER_S_OK) continue;
-                if (tver[j] > t->opts.early_cut * ref_ns) cut[j] = 1;
-                else if (tver[j] > kLightFactor * ref_ns) {
-                    reps[j] = std::min(R, 3);
-                    warm[j] = std::min(W, 1);
-                }
-            }
-        }
-
-        // ---- phase 2: timing
-        std::vector<cudaGraphExec_t> execs(n, nullptr);
-        std::vector<int> number(n, 1);
-        const size_t tb = 2 * n;  // timing events start here
-        // nwin back-to-back windows of `num` launches each, bracketed by events ev[b..b+nwin]:
-        // a graph of G <= 8 launches replayed L times per window (few nodes to capture and
-        // instantiate on the host, back-to-back launches on the device); returns G * L
-        auto time_windows = [&](size_t j, int num, int nwin, size_t b, int& used) -> tuner_status {
-            const int G = std::min(num, kMaxGraphNodes);
-            const int L = (num + G - 1) / G;
-            used = G * L;
-            LaunchCtx cc = ctx;
-            cc.stream = cap;
-            set_capturing(true);
-            cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
-            for (int i = 0; i < G && e == cudaSuccess; ++i) e = fn[j](cc);
-            cudaGraph_t g = nullptr;
-            cudaError_t e2 = cudaStreamEndCapture(cap, &g);
-            set_capturing(false);
-            if (e != cudaSuccess) return cuda_fail(e, "graph capture");
-            if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamEndCapture");
-            e = exec_for(g, execs[j]);
-            cudaGraphDestroy(g);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-            CU(cudaEventRecord(ev[b], st));
-            for (int r = 0; r < nwin; ++r) {
-                for (int l = 0; l < L; ++l) CU(cudaGraphLaunch(execs[j], st));
-                count_launches(used);
-                CU(cudaEventRecord(ev[b + r + 1], st));
-            }
-            return TUNER_OK;
-        };
+    // phase 2: W warm-ups + R repeat windows per candidate that is not cut
+    tuner_status phase_time(Batch& b, std::vector<Result>& out) {
+        const size_t n = b.n;
+        const int R = t->opts.repeats;
+        auto& ev = event_pool(dev);
+        b.prog.clear();
         for (size_t j = 0; j < n; ++j) {
-            if (out[j].status != TUNER_S_OK || cut[j]) continue;
-            set_knobs(j);
+            if (out[j].status != TUNER_S_OK || b.cut[j]) continue;
+            set_knobs(b, j);
             int num = t->opts.number;
             if (num <= 0) {
-                double want = 20000.0 / std::max(tver[j], 1.0);
+                double want = 20000.0 / std::max(b.tver[j], 1.0);
                 num = (int)std::min(100.0, std::max(1.0, std::ceil(want)));
             }
-            for (int i = 0; i < warm[j]; ++i) {
-                cudaError_t e = fn[j](ctx);
+            for (int i = 0; i < b.warm[j]; ++i) {
+                cudaError_t e = b.fn[j](b.ctx);
                 if (e != cudaSuccess) return cuda_fail(e, "warm-up launch");
             }
-            tuner_status ts = time_windows(j, num, reps[j], tb + j * EB, number[j]);
+            tuner_status ts = time_windows(b, j, num, b.reps[j], b.tb + j * b.EB, b.number[j]);
             if (ts != TUNER_OK) return ts;
         }
+        tuner_status s = wait_progress(b.prog, b.stall_ms);
+        if (s != TUNER_OK) return s;
         cudaError_t se = cudaStreamSynchronize(st);
         for (auto ge : transient) cudaGraphExecDestroy(ge);
         transient.clear();
@@ -371,18 +460,18 @@ struct GpuMeasurer : Measurer {
                 out[j].cost_ns = INFINITY;
                 continue;
             }
-            if (cut[j]) {
-                out[j].cost_ns = tver[j];
+            if (b.cut[j]) {
+                out[j].cost_ns = b.tver[j];
                 out[j].nsamp = 1;
-                out[j].samp[0] = (float)tver[j];
+                out[j].samp[0] = (float)b.tver[j];
                 continue;
             }
-            const size_t b = tb + j * EB;
-            const int Rj = reps[j];
+            const size_t base = b.tb + j * b.EB;
+            const int Rj = b.reps[j];
             for (int r = 0; r < Rj; ++r) {
                 float ms = 0.f;
-                CU(cudaEventElapsedTime(&ms, ev[b + r], ev[b + r + 1]));
-                per[r] = (double)ms * 1e6 / number[j];
+                CU(cudaEventElapsedTime(&ms, ev[base + r], ev[base + r + 1]));
+                per[r] = (double)ms * 1e6 / b.number[j];
             }
             // R-M2: trimmed mean (drop the fastest and slowest repeat) for R >= 5, median for
             // R < 5 -- the device timer ticks in ~1 us steps, so a plain median of 20 us
@@ -398,45 +487,135 @@ struct GpuMeasurer : Measurer {
                 out[j].cost_ns = (Rj % 2) ? per[Rj / 2] : 0.5 * (per[Rj / 2 - 1] + per[Rj / 2]);
             }
         }
+        return TUNER_OK;
+    }
 
-        // ---- phase 3 (R-M4): long windows for the candidates near the best known cost
-        if (t->opts.early_cut > 0.0 && t->opts.number <= 0) {
-            double best = best_coarse;
-            for (size_t j = 0; j < n; ++j)
-                if (out[j].status == TUNER_S_OK && !cut[j]) best = std::min(best, out[j].cost_ns);
-            best_coarse = best;
-            std::vector<char> precise(n, 0);
-            std::vector<int> nlong(n, 0);
-            bool any = false;
-            for (size_t j = 0; j < n; ++j) {
-                if (out[j].status != TUNER_S_OK || cut[j] || !(out[j].cost_ns <= kPreciseFactor * best)) continue;
-                precise[j] = 1;
-                any = true;
-                set_knobs(j);
-                const double want = kPreciseWindowNs / std::max(out[j].cost_ns, 1.0);
-                const int num = (int)std::min(4000.0, std::max(1.0, std::ceil(want)));
-                tuner_status ts = time_windows(j, num, kPreciseWindows, tb + j * EB + (size_t)reps[j], nlong[j]);
-                if (ts != TUNER_OK) return ts;
+    // phase 3 (R-M4): long windows for the candidates near the best coarse cost `best`
+    tuner_status phase_precise(Batch& b, std::vector<Result>& out, double best) {
+        const size_t n = b.n;
+        auto& ev = event_pool(dev);
+        bool any = false;
+        b.prog.clear();
+        for (size_t j = 0; j < n; ++j) {
+            if (out[j].status != TUNER_S_OK || b.cut[j] || !(out[j].cost_ns <= kPreciseFactor * best)) continue;
+            b.precise[j] = 1;
+            any = true;
+            set_knobs(b, j);
+            const double want = kPreciseWindowNs / std::max(out[j].cost_ns, 1.0);
+            const int num = (int)std::min(4000.0, std::max(1.0, std::ceil(want)));
+            tuner_status ts = time_windows(b, j, num, kPreciseWindows, b.tb + j * b.EB + (size_t)b.reps[j], b.nlong[j]);
+            if (ts != TUNER_OK) return ts;
+        }
+        if (!any) return TUNER_OK;
+        tuner_status s = wait_progress(b.prog, b.stall_ms);
+        if (s != TUNER_OK) return s;
+        cudaError_t se3 = cudaStreamSynchronize(st);
+        for (auto ge : transient) cudaGraphExecDestroy(ge);
+        transient.clear();
+        if (se3 != cudaSuccess) return cuda_fail(se3, "cudaStreamSynchronize (precise timing)");
+        for (size_t j = 0; j < n; ++j) {
+            if (!b.precise[j]) continue;
+            const size_t base = b.tb + j * b.EB + (size_t)b.reps[j];
+            double sum = 0.0;
+            for (int r = 0; r < kPreciseWindows; ++r) {
+                float ms = 0.f;
+                CU(cudaEventElapsedTime(&ms, ev[base + r], ev[base + r + 1]));
+                sum += (double)ms * 1e6 / b.nlong[j];
             }
-            if (any) {
-                cudaError_t se3 = cudaStreamSynchronize(st);
-                for (auto ge : transient) cudaGraphExecDestroy(ge);
-                transient.clear();
-                if (se3 != cudaSuccess) return cuda_fail(se3, "cudaStreamSynchronize (precise timing)");
-                for (size_t j = 0; j < n; ++j) {
-                    if (!precise[j]) continue;
-                    const size_t b = tb + j * EB + (size_t)reps[j];
-                    double sum = 0.0;
-                    for (int r = 0; r < kPreciseWindows; ++r) {
-                        float ms = 0.f;
-                        CU(cudaEventElapsedTime(&ms, ev[b + r], ev[b + r + 1]));
-                        sum += (double)ms * 1e6 / nlong[j];
-                    }
-                    out[j].cost_ns = sum / kPreciseWindows;
+            out[j].cost_ns = sum / kPreciseWindows;
+        }
+        return TUNER_OK;
+    }
+
+    // SPMD tiers (R-M1, R-M3, R-M4): the early-cut and precise-tier
+    // references are minima over ALL ranks (a 16-byte all-gather after the verify phase and
+    // one after the repeat phase), so the tier a candidate gets depends only on its own times
+    // and on values every rank agrees on -- never on the rank it landed on.  A rank's local
+    // failure travels through the same all-gathers, so all ranks fail together instead of
+    // leaving the others blocked in a collective.
+    tuner_status agree_min(bool coll, double& v, tuner_status local) {
+        if (!coll) return local;
+        struct Pair {
+            double v;
+            int32_t st, pad;
+        };
+        const int G = t->opts.world;
+        Pair send{v, (int32_t)local, 0};
+        std::vector<Pair> recv(G);
+        tuner_status c = t->comm->allgather(&send, recv.data(), (int64_t)sizeof(Pair));
+        if (c != TUNER_OK) return c;
+        t->stats.collectives++;
+        int32_t bad = TUNER_OK;
+        for (const Pair& q : recv) {
+            if (q.v < v) v = q.v;
+            if (q.st != TUNER_OK) bad = q.st;
+        }
+        if (local != TUNER_OK) return local;
+        if (bad != TUNER_OK) return fail((tuner_status)bad, "another rank failed while measuring this batch");
+        return TUNER_OK;
+    }
+
+    // `collective` = false: rank 0 alone re-times a winner found on another rank (§8(e)); it
+    // reads the shared tier references but never updates them (they stay identical on all ranks)
+    tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out, double incumbent,
+                         bool collective) override {
+        (void)incumbent;
+        Batch b;
+        const size_t n = b.n = pts.size();
+        out.assign(n, Result{});
+        const bool tiers = t->opts.early_cut > 0.0;
+        const bool coll = collective && tiers && t->comm && t->opts.world > 1;
+        if (n == 0 && !coll) return TUNER_OK;
+        b.fn.assign(n, nullptr);
+        b.rk.assign(n, RuntimeKnobs{});
+        b.launched.assign(n, 0);
+        b.cut.assign(n, 0);
+        b.precise.assign(n, 0);
+        b.tver.assign(n, 0.0);
+        b.reps.assign(n, t->opts.repeats);
+        b.warm.assign(n, t->opts.warmup);
+        b.number.assign(n, 1);
+        b.nlong.assign(n, 0);
+        b.execs.assign(n, nullptr);
+        b.stall_ms = std::max(5000.0, 4.0 * t->opts.timeout_ms);
+
+        tuner_status s = n ? phase_verify(pts, b, out) : TUNER_OK;
+        // early cut (SURVEY d.5, R-M3): rank hopeless candidates by their verify run and time
+        // clearly non-competitive ones (> 1.5x) with 3 repeats instead of R
+        double vmin = INFINITY;
+        if (s == TUNER_OK)
+            for (size_t j = 0; j < n; ++j)
+                if (out[j].status == TUNER_S_OK) vmin = std::min(vmin, b.tver[j]);
+        if ((s = agree_min(coll, vmin, s)) != TUNER_OK) return s;
+        if (tiers) {
+            const double ref_ns = std::min(best_tver, vmin);
+            if (collective) best_tver = ref_ns;
+            for (size_t j = 0; j < n; ++j) {
+                if (out[j].status != TUNER_S_OK) continue;
+                if (b.tver[j] > t->opts.early_cut * ref_ns) {
+                    b.cut[j] = 1;
+                    t->stats.early_cut++;
+                } else if (b.tver[j] > kLightFactor * ref_ns) {
+                    b.reps[j] = std::min(t->opts.repeats, 3);
+                    b.warm[j] = std::min(t->opts.warmup, 1);
+                    t->stats.light++;
                 }
             }
         }
-        return TUNER_OK;
+        s = n ? phase_time(b, out) : TUNER_OK;
+        const bool tier3 = tiers && t->opts.number <= 0;
+        double cmin = INFINITY;
+        if (s == TUNER_OK)
+            for (size_t j = 0; j < n; ++j)
+                if (out[j].status == TUNER_S_OK && !b.cut[j]) cmin = std::min(cmin, out[j].cost_ns);
+        if ((s = agree_min(coll && tier3, cmin, s)) != TUNER_OK) return s;
+        if (!tier3) return TUNER_OK;
+        const double best = std::min(best_coarse, cmin);
+        if (collective) best_coarse = best;
+        if (n == 0) return TUNER_OK;
+        s = phase_precise(b, out, best);
+        for (size_t j = 0; j < n; ++j) t->stats.precise += b.precise[j];
+        return s;
     }
 };
 }  // namespace
@@ -450,16 +629,21 @@ tuner_status make_gpu_measurer(Tuner* t, std::unique_ptr<Measurer>& out) {
     return TUNER_OK;
 }
 
-tuner_status gpu_kernel_run(const Tuner* t, const Pt& p, const tuner_buffers* buf, void* stream) {
+tuner_status gpu_kernel_run(Tuner* t, const Pt& p, const tuner_buffers* buf, void* stream) {
     RuntimeKnobs rk;
     LaunchFn fn = resolve(t, p, rk);
     if (!fn) return fail(TUNER_ERANGE, "schedule not compiled");
+    if (rk.sched >= 1) {
+        tuner_status s = ensure_streamk(t, (cudaStream_t)stream);
+        if (s != TUNER_OK) return s;
+    }
     int nsm = 148, dev = 0;
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     LaunchCtx ctx{&t->info, buf->x, buf->w, buf->y, rk.split, rk.vec, rk.stages, rk.sched, (cudaStream_t)stream, nsm};
     for (int d = 0; d < 3; ++d) ctx.dims[d] = rk.dims[d];
     ctx.raster = rk.raster;
+    ctx.sk = &t->sk;
     CU(fn(ctx));
     return TUNER_OK;
 }

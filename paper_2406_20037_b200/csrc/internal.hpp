@@ -3,6 +3,7 @@
 #include <array>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -98,9 +99,11 @@ tuner_status nccl_unique_id(void* out128);
 // ---------------------------------------------------------------- measurement backends
 struct Measurer {
     virtual ~Measurer() = default;
-    // measure `pts` (this rank's share of a batch) -> results in the same order
-    // `incumbent` = best cost measured so far (for the early cut)
-    virtual tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out, double incumbent) = 0;
+    // measure `pts` (this rank's share of a batch) -> results in the same order.
+    // `incumbent` = best cost measured so far; `collective` = every rank is in this call
+    // (the batch's shard), false = one rank re-times alone (calibration)
+    virtual tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out, double incumbent,
+                                 bool collective) = 0;
     virtual bool valid(const Pt& p) = 0;
 };
 
@@ -108,7 +111,7 @@ struct Tuner;
 std::unique_ptr<Measurer> make_table_measurer(Tuner* t, std::vector<double>&& table, const double* samples,
                                               int nsamp);
 tuner_status make_gpu_measurer(Tuner* t, std::unique_ptr<Measurer>& out);
-tuner_status gpu_kernel_run(const Tuner* t, const Pt& p, const tuner_buffers* buf, void* stream);
+tuner_status gpu_kernel_run(Tuner* t, const Pt& p, const tuner_buffers* buf, void* stream);
 tuner_status gpu_reference(const Tuner* t, const tuner_buffers* buf, float* y_ref, float* y_absref,
                            void* stream);
 extern std::atomic<int64_t>* g_launch_counter_ptr();
@@ -132,6 +135,12 @@ struct Tuner {
     tuner_stats stats{};
     double best_cost = INFINITY;
     uint64_t grid_cursor = 0;  // next union linear id tuner_grid examines
+    StreamKScratch sk;         // stream-K workspace (tcgen05 SCHED >= 1), allocated on first need
+
+    Tuner() = default;
+    Tuner(const Tuner&) = delete;
+    Tuner& operator=(const Tuner&) = delete;
+    ~Tuner();  // harness.cu: drops the measurer (device synchronised), then frees `sk`
 
     uint64_t linear(const Pt& p) const;
     Pt from_public(const tuner_point& tp, tuner_status& st) const;  // validates dims/ranges
@@ -142,7 +151,14 @@ struct Tuner {
     bool measured(const Pt& p) const { return memo.count(linear(p)) != 0; }
     double cost(const Pt& p) const { return history[memo.at(linear(p))].cost_ns; }
 
+    std::FILE* trial_log = nullptr;  // append-only JSONL log (opts.trial_log), rank 0 writes
+    std::string key;                 // the problem key of the log lines (op, shape, dtype)
+
     tuner_status measure_batch(const std::vector<Pt>& batch);
+    tuner_status calibrate(const std::vector<Pt>& batch, std::vector<Result>& res);
+    void record(const Pt& p, const tuner_result& smp, std::vector<float>&& samples, bool log);
+    void log_trial(const Pt& p, const tuner_result& smp, const std::vector<float>& samples);
+    tuner_status replay_log(const char* path);
     tuner_status draw(int32_t n, std::vector<Pt>& out);
     tuner_status measure_chunked(const std::vector<Pt>& pts);
     tuner_status evolve(int32_t n, int32_t pop, int32_t elite, std::vector<Pt>& out);

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "../shape.hpp"
@@ -22,6 +23,7 @@ struct LaunchCtx {
     int num_sms;
     int dims[3] = {1, 1, 1};  // runtime thread-block shape knobs (depthwise: CT, QT, PT)
     int raster = 0;           // runtime tile order (tcgen05): 0 = M fastest, 1 = N fastest
+    const StreamKScratch* sk = nullptr;  // stream-K workspace of the launching handle (SCHED >= 1)
 };
 
 typedef cudaError_t (*LaunchFn)(const LaunchCtx&);
@@ -34,6 +36,21 @@ LaunchFn registry_find(uint64_t key);
 // Counter of candidate-kernel launches (graph nodes included).
 void count_launches(int64_t n);
 void set_capturing(bool on);
+
+// Dynamic shared-memory opt-in (cudaFuncAttributeMaxDynamicSharedMemorySize) once per
+// (kernel instantiation, device): the attribute is per device, so a process driving several
+// devices sets it on each (one bit per device ordinal < 64 in the instantiation's mask).
+template <typename K>
+inline cudaError_t smem_optin(std::atomic<unsigned long long>& mask, K kern, int bytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
 
 // Split-K zeroing as a kernel that lets the partial-sum kernel launch early (programmatic
 // dependent launch): the dependent kernel stages and multiplies while Y is being zeroed and

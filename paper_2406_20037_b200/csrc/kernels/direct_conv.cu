@@ -165,11 +165,10 @@ __global__ void __launch_bounds__(direct_max_threads(KT, TP)) direct_conv_kernel
 template <typename TIn, int KT, int TP>
 cudaError_t direct_launch(const LaunchCtx& c) {
     auto kern = direct_conv_kernel<TIn, KT, TP>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    static std::atomic<unsigned long long> optin{0};
+    {
+        cudaError_t e = smem_optin(optin, kern, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     const ShapeInfo& s = *c.sh;
     DirectParams p;

@@ -276,11 +276,10 @@ cudaError_t dwconv_win_launch(const LaunchCtx& c) {
 template <typename TIn, int VEC, int TQ, bool SMEM>
 cudaError_t dwconv_launch(const LaunchCtx& c) {
     auto kern = dwconv_kernel<TIn, VEC, TQ, SMEM>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    static std::atomic<unsigned long long> optin{0};
+    {
+        cudaError_t e = smem_optin(optin, kern, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     const ShapeInfo& s = *c.sh;
     const int ct = c.dims[0], qt = c.dims[1], pt = c.dims[2];

@@ -372,11 +372,10 @@ template <int BM, int BN, int BK, int TT, int UNROLL, bool CONV, typename TIn = 
 cudaError_t simt_launch(const LaunchCtx& c) {
     using Cfg = SimtCfg<BM, BN, BK, TT>;
     auto kern = simt_gemm_f32_kernel<BM, BN, BK, TT, UNROLL, CONV, TIn>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    static std::atomic<unsigned long long> optin{0};
+    {
+        cudaError_t e = smem_optin(optin, kern, (int)Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     const ShapeInfo& s = *c.sh;
     SimtParams p;

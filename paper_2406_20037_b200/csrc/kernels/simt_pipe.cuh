@@ -314,11 +314,10 @@ template <int BM, int BN, int BK, int TT, int KW, int VW, bool CONV>
 cudaError_t pipe_launch(const LaunchCtx& c) {
     constexpr int NT = (BM / TT) * (BN / TT) * KW;
     auto kern = simt_pipe_kernel<BM, BN, BK, TT, KW, VW, CONV>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    static std::atomic<unsigned long long> optin{0};
+    {
+        cudaError_t e = smem_optin(optin, kern, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     const ShapeInfo& s = *c.sh;
     PipeParams p;

@@ -42,7 +42,6 @@
 
 namespace db200 {
 
-static constexpr int kStreamKSlots = 1024;  // (group, CTA) workspace slots of a stream-K launch
 
 template <int BN, int BK, int STAGES, int CG>
 struct TcCfg {
@@ -546,30 +545,44 @@ static bool encode_f32(CUtensorMap* m, void* ptr, int rank, const cuuint64_t* di
     return r == CUDA_SUCCESS;
 }
 
-// stream-K scratch, per device, allocated once (outside graph capture: the first
-// launch of a schedule is never captured): kStreamKSlots flags, zeroed once and
-// left at 0 by every launch (heads re-arm their tails' flags), and one
-// 128 x 256 fp32 partial-accumulator slot per (group, CTA), thread-major
-// ([16-column group][row][16]) so parking and fix-up are coalesced
-static bool stream_k_scratch(unsigned** flags, float** ws) {
-    static unsigned* fl[64] = {};
-    static float* w[64] = {};
+// Co-resident CTA groups of an instantiation on the current device (computed once per device):
+// cudaOccupancyMaxActiveClusters with the launch's block, dynamic shared memory and cluster
+// shape (it accounts for the ~240 registers per thread of these kernels), capped by TMEM
+// (512 columns per SM) and by the shared-memory bound; never more than one group per CG SMs
+// times that.
+template <int BN, int BK, int STAGES, int TQ, int CG>
+static long long tc_resident_groups(int num_sms) {
+    using Cfg = TcCfg<BN, BK, STAGES, CG>;
+    static std::atomic<long long> cache[64];
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return false;
-    dev &= 63;
-    if (!fl[dev]) {
-        unsigned* f = nullptr;
-        float* b = nullptr;
-        if (cudaMalloc(&f, kStreamKSlots * sizeof(unsigned)) != cudaSuccess) return false;
-        if (cudaMemset(f, 0, kStreamKSlots * sizeof(unsigned)) != cudaSuccess) return false;
-        if (cudaMalloc(&b, (size_t)kStreamKSlots * 128 * 256 * sizeof(float)) != cudaSuccess) return false;
-        if (cudaDeviceSynchronize() != cudaSuccess) return false;
-        fl[dev] = f;
-        w[dev] = b;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    long long v = cache[dev & 63].load(std::memory_order_relaxed);
+    if (v > 0) return v;
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(CG);
+    cfg.blockDim = dim3(Cfg::THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, tc_gemm_bf16_kernel<BN, BK, STAGES, TQ, CG>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        clusters = 0;
     }
-    *flags = fl[dev];
-    *ws = w[dev];
-    return true;
+    int per_sm = (int)((228 * 1024) / (Cfg::SMEM + 1024));
+    const int tmem_per_sm = (int)(512 / Cfg::TMEM_COLS);
+    per_sm = per_sm < tmem_per_sm ? per_sm : tmem_per_sm;
+    per_sm = per_sm < 1 ? 1 : per_sm;
+    long long g = (long long)(num_sms / CG) * per_sm;
+    if (clusters > 0 && clusters < g) g = clusters;
+    cache[dev & 63].store(g, std::memory_order_relaxed);
+    return g;
 }
 
 // 3-D K-major operand [batch][rows][K] -> box {64, box_rows, 1}
@@ -586,11 +599,10 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     using Cfg = TcCfg<BN, BK, STAGES, CG>;
     constexpr bool CONV = TQ > 0;
     auto kern = tc_gemm_bf16_kernel<BN, BK, STAGES, TQ, CG>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    static std::atomic<unsigned long long> optin{0};
+    {
+        cudaError_t e = smem_optin(optin, kern, (int)Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     const ShapeInfo& s = *c.sh;
     CUtensorMap ta, tb;
@@ -663,17 +675,18 @@ cudaError_t tc_launch(const LaunchCtx& c) {
         cudaError_t e = zero_for_splitk((float*)c.y, s.y_elems, c.stream);
         if (e != cudaSuccess) return e;
     }
-    // persistent grid: CTA groups = SMs / CG x resident slots (shared memory and TMEM limited);
-    // every group must be co-resident for the stream-K flag protocol
-    int per_sm = (int)((228 * 1024) / (Cfg::SMEM + 1024));
-    per_sm = per_sm < 1 ? 1 : per_sm;
-    const int tmem_per_sm = (int)(512 / Cfg::TMEM_COLS);
-    per_sm = per_sm < tmem_per_sm ? per_sm : tmem_per_sm;
-    long long groups = (long long)(c.num_sms / CG) * per_sm;
+    // persistent grid: as many CTA groups as can be co-resident (the stream-K flag protocol
+    // spins heads on their tails, so every group MUST be resident at once): the occupancy
+    // calculator's active clusters (registers, shared memory, cluster shape) capped by TMEM
+    const long long groups_max = tc_resident_groups<BN, BK, STAGES, TQ, CG>(c.num_sms);
+    if (groups_max < 1) return cudaErrorInvalidConfiguration;
+    long long groups = groups_max;
     if (c.sched >= 1) {
-        if (!stream_k_scratch(&p.flags, &p.ws)) return cudaErrorMemoryAllocation;
+        if (!c.sk || !c.sk->flags || !c.sk->ws) return cudaErrorInvalidValue;  // the handle owns the workspace
+        p.flags = c.sk->flags;
+        p.ws = c.sk->ws;
         if (groups > p.total_iters) groups = p.total_iters;
-        if (groups * CG > kStreamKSlots) groups = kStreamKSlots / CG;
+        if (groups * CG > c.sk->slots) groups = c.sk->slots / CG;
         if (c.sched == 2) {  // whole waves tile by tile; the remainder tiles cut into equal k-chunks,
                              // one chunk per group (groups without one stop after their waves)
             p.dp_tiles = (int)((tiles / groups) * groups);

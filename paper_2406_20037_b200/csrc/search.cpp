@@ -7,11 +7,14 @@
 // Droplet cap of 100 trials.  Readings R-xx: DESIGN.md §3.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <unordered_set>
 
 #include "internal.hpp"
+#include "nvtx.hpp"
 
 namespace db200 {
 
@@ -98,8 +101,29 @@ struct Slot {  // 96 bytes, keyed by batch index so results are rank-independent
 static_assert(sizeof(Slot) == 96, "slot layout");
 }  // namespace
 
+static void slot_from(Slot& d, int32_t idx, int32_t rank, const Result& r) {
+    std::memset(&d, 0, sizeof(Slot));
+    d.idx = idx;
+    d.rank = rank;
+    d.status = r.status;
+    d.cost_ns = r.cost_ns;
+    d.max_err = r.max_err;
+    d.nsamp = r.nsamp;
+    std::memcpy(d.samp, r.samp, sizeof(d.samp));
+}
+static void result_from(Result& x, const Slot& s) {
+    x.cost_ns = s.cost_ns;
+    x.max_err = s.max_err;
+    x.status = s.status;
+    x.rank = s.rank;
+    x.nsamp = s.nsamp < 0 ? 0 : (s.nsamp > kMaxSamples ? kMaxSamples : s.nsamp);
+    std::memcpy(x.samp, s.samp, sizeof(x.samp));
+}
+static constexpr int32_t kSlotError = -2;  // a slot carrying a rank's failure (status = the error)
+
 tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
     if (batch.empty()) return TUNER_OK;
+    NvtxRange nv("measure_batch");
     auto t0 = std::chrono::steady_clock::now();
     const int G = opts.world > 1 ? opts.world : 1;
     const int r = opts.world > 1 ? opts.rank : 0;
@@ -111,46 +135,42 @@ tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
     }
     std::vector<Result> lres;
     const int64_t launches0 = g_launch_counter_ptr()->load();
-    tuner_status st = measurer->measure(local, lres, best_cost);
+    tuner_status st = measurer->measure(local, lres, best_cost, true);
     stats.kernel_launches += g_launch_counter_ptr()->load() - launches0;
-    if (st != TUNER_OK) return st;
     for (auto& x : lres) x.rank = r;
     std::vector<Result> res(batch.size());
     if (!comm) {
+        if (st != TUNER_OK) return st;
         res = lres;
     } else {
+        // every rank takes part in the all-gather even after a local failure (its slot 0
+        // then carries the error), so a failing rank never leaves the others blocked
         const size_t per = (batch.size() + G - 1) / G;
         std::vector<Slot> send(per), recv(per * G);
         for (size_t i = 0; i < per; ++i) {
             std::memset(&send[i], 0, sizeof(Slot));
             send[i].idx = -1;
             send[i].rank = r;
-            if (i < lres.size()) {
-                send[i].idx = local_idx[i];
-                send[i].status = lres[i].status;
-                send[i].cost_ns = lres[i].cost_ns;
-                send[i].max_err = lres[i].max_err;
-                send[i].nsamp = lres[i].nsamp;
-                std::memcpy(send[i].samp, lres[i].samp, sizeof(send[i].samp));
-            }
+            if (st == TUNER_OK && i < lres.size()) slot_from(send[i], local_idx[i], r, lres[i]);
         }
-        st = comm->allgather(send.data(), recv.data(), (int64_t)(per * sizeof(Slot)));
+        if (st != TUNER_OK) {
+            send[0].idx = kSlotError;
+            send[0].status = st;
+        }
+        tuner_status cs = comm->allgather(send.data(), recv.data(), (int64_t)(per * sizeof(Slot)));
         if (st != TUNER_OK) return st;
+        if (cs != TUNER_OK) return cs;
         stats.collectives++;
         size_t filled = 0;
         for (const Slot& s : recv) {
+            if (s.idx == kSlotError) return fail((tuner_status)s.status, "another rank failed while measuring");
             if (s.idx < 0) continue;
             if ((size_t)s.idx >= batch.size()) return fail(TUNER_ENCCL, "corrupt all-gather slot");
-            Result& x = res[s.idx];
-            x.cost_ns = s.cost_ns;
-            x.max_err = s.max_err;
-            x.status = s.status;
-            x.rank = s.rank;
-            x.nsamp = s.nsamp < 0 ? 0 : (s.nsamp > kMaxSamples ? kMaxSamples : s.nsamp);
-            std::memcpy(x.samp, s.samp, sizeof(x.samp));
+            result_from(res[s.idx], s);
             ++filled;
         }
         if (filled != batch.size()) return fail(TUNER_ENCCL, "all-gather returned an incomplete batch");
+        if (G > 1 && !table_mode && (st = calibrate(batch, res)) != TUNER_OK) return st;
     }
     for (size_t j = 0; j < batch.size(); ++j) {
         tuner_result smp;
@@ -160,16 +180,186 @@ tuner_status Tuner::measure_batch(const std::vector<Pt>& batch) {
         smp.cost_ns = res[j].status == TUNER_S_OK ? res[j].cost_ns : INFINITY;
         smp.max_err = res[j].max_err;
         smp.rank = res[j].rank;
-        memo[linear(batch[j])] = history.size();
-        history.push_back(smp);
-        hsamples.emplace_back(res[j].samp, res[j].samp + res[j].nsamp);
-        if (smp.cost_ns < best_cost) best_cost = smp.cost_ns;
+        record(batch[j], smp, std::vector<float>(res[j].samp, res[j].samp + res[j].nsamp), true);
     }
     stats.candidates += (int64_t)batch.size();
     stats.batches++;
     stats.measure_wall_ns +=
         std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count();
     return TUNER_OK;
+}
+
+// Per-GPU calibration ("a winner found on rank r is re-timed on rank 0 before
+// acceptance"): the batch's first argmin, when it beats the incumbent and was timed on another
+// rank, is re-timed on rank 0 (with the precise tier) and rank 0's cost replaces it; repeated,
+// at most kCalibrations times per batch, while the new argmin is another such winner.  So every
+// incumbent's cost -- every point Droplet or best-of-N accepts -- is a rank-0 cost, and no GPU's
+// bias decides an acceptance.  The re-timing result travels in one all-gather (rank 0's slot).
+tuner_status Tuner::calibrate(const std::vector<Pt>& batch, std::vector<Result>& res) {
+    static constexpr int kCalibrations = 4;
+    const int G = opts.world;
+    std::vector<char> done(batch.size(), 0);
+    for (int it = 0; it < kCalibrations; ++it) {
+        size_t js = batch.size();
+        for (size_t j = 0; j < batch.size(); ++j)
+            if (res[j].status == TUNER_S_OK && (js == batch.size() || res[j].cost_ns < res[js].cost_ns)) js = j;
+        if (js == batch.size() || !(res[js].cost_ns < best_cost) || res[js].rank == 0 || done[js]) break;
+        done[js] = 1;
+        Slot send;
+        std::memset(&send, 0, sizeof(send));
+        send.idx = -1;
+        if (opts.rank == 0) {
+            std::vector<Result> rr;
+            tuner_status ms = measurer->measure(std::vector<Pt>{batch[js]}, rr, best_cost, false);
+            if (ms == TUNER_OK) {
+                slot_from(send, (int32_t)js, 0, rr[0]);
+            } else {
+                send.idx = kSlotError;
+                send.status = ms;
+            }
+        }
+        std::vector<Slot> recv(G);
+        tuner_status cs = comm->allgather(&send, recv.data(), (int64_t)sizeof(Slot));
+        if (cs != TUNER_OK) return cs;
+        stats.collectives++;
+        if (recv[0].idx == kSlotError) return fail((tuner_status)recv[0].status, "rank 0 failed re-timing a winner");
+        if (recv[0].idx != (int32_t)js) return fail(TUNER_ENCCL, "corrupt calibration slot");
+        result_from(res[js], recv[0]);
+        stats.calibrations++;
+    }
+    return TUNER_OK;
+}
+
+// Append one measured (or replayed) point to the history and the memo; log it (rank 0).
+void Tuner::record(const Pt& p, const tuner_result& smp, std::vector<float>&& samples, bool log) {
+    memo[linear(p)] = history.size();
+    history.push_back(smp);
+    hsamples.push_back(std::move(samples));
+    if (smp.cost_ns < best_cost) best_cost = smp.cost_ns;
+    if (log && trial_log && opts.rank == 0) log_trial(p, smp, hsamples.back());
+}
+
+// ---------------------------------------------------------------- trial log
+// One JSON object per line:
+//   {"key":"<op/shape/dtype>","sketch":S,"vals":[v0,...],"cost_ns":C|null,"max_err":E,"status":s,
+//    "rank":r,"samp":[t0,...]}
+// Knob VALUES (not indices) are logged, so a log replays into a tuner whose value lists differ;
+// lines of another problem or sketch, or with a value outside this tuner's lists, are skipped.
+static std::string problem_key(int32_t op, const tuner_shape& s) {
+    char buf[320];
+    std::snprintf(buf, sizeof buf,
+                  "op%d/dt%d/b%lld/m%lld/n%lld/k%lld/N%lld/C%lld/H%lld/W%lld/K%lld/R%lld/S%lld/st%d.%d/pd%d.%d/dl%d.%d",
+                  op, s.dtype, (long long)s.b, (long long)s.m, (long long)s.n, (long long)s.k, (long long)s.N,
+                  (long long)s.C, (long long)s.H, (long long)s.W, (long long)s.K, (long long)s.R, (long long)s.S,
+                  s.stride_h, s.stride_w, s.pad_h, s.pad_w, s.dil_h, s.dil_w);
+    return buf;
+}
+
+void Tuner::log_trial(const Pt& p, const tuner_result& smp, const std::vector<float>& samples) {
+    int32_t v[TUNER_MAX_KNOBS];
+    values_of(p, v);
+    std::string line = "{\"key\":\"" + key + "\",\"sketch\":" + std::to_string(spaces[p.pos].sketch) + ",\"vals\":[";
+    for (int d = 0; d < p.n; ++d) line += (d ? "," : "") + std::to_string(v[d]);
+    char num[64];
+    line += "],\"cost_ns\":";
+    if (std::isfinite(smp.cost_ns)) {
+        std::snprintf(num, sizeof num, "%.17g", smp.cost_ns);
+        line += num;
+    } else {
+        line += "null";
+    }
+    std::snprintf(num, sizeof num, "%.9g", smp.max_err);
+    line += ",\"max_err\":" + std::string(num) + ",\"status\":" + std::to_string(smp.status) +
+            ",\"rank\":" + std::to_string(smp.rank) + ",\"samp\":[";
+    for (size_t i = 0; i < samples.size(); ++i) {
+        std::snprintf(num, sizeof num, "%.9g", (double)samples[i]);
+        line += (i ? "," : "") + std::string(num);
+    }
+    line += "]}\n";
+    std::fwrite(line.data(), 1, line.size(), trial_log);
+    std::fflush(trial_log);
+}
+
+// the numbers of a JSON array "[a,b,...]" starting at p (after the '['); returns past ']'
+static const char* parse_array(const char* p, std::vector<double>& out) {
+    out.clear();
+    while (*p == ' ') ++p;
+    if (*p == ']') return p + 1;
+    for (;;) {
+        char* e = nullptr;
+        const double x = std::strtod(p, &e);
+        if (e == p) return nullptr;
+        out.push_back(x);
+        p = e;
+        while (*p == ' ') ++p;
+        if (*p == ']') return p + 1;
+        if (*p != ',') return nullptr;
+        ++p;
+    }
+}
+static const char* field(const char* line, const char* name) {
+    const char* f = std::strstr(line, name);
+    return f ? f + std::strlen(name) : nullptr;
+}
+
+tuner_status Tuner::replay_log(const char* path) {
+    std::FILE* f = std::fopen(path, "r");
+    if (!f) return TUNER_OK;  // no log yet: a fresh job
+    std::string line;
+    char buf[4096];
+    int64_t lineno = 0;
+    tuner_status st = TUNER_OK;
+    std::vector<double> vals, samp;
+    while (st == TUNER_OK && std::fgets(buf, sizeof buf, f)) {
+        line.assign(buf);
+        while (!line.empty() && line.back() != '\n' && std::fgets(buf, sizeof buf, f)) line += buf;
+        ++lineno;
+        if (line.find_first_not_of(" \t\r\n") == std::string::npos) continue;
+        const char* L = line.c_str();
+        const char* k = field(L, "\"key\":\"");
+        const char* sk = field(L, "\"sketch\":");
+        const char* va = field(L, "\"vals\":[");
+        const char* co = field(L, "\"cost_ns\":");
+        const char* me = field(L, "\"max_err\":");
+        const char* ss = field(L, "\"status\":");
+        const char* rk = field(L, "\"rank\":");
+        const char* sa = field(L, "\"samp\":[");
+        if (!k || !sk || !va || !co || !me || !ss || !rk || !sa || !parse_array(va, vals) || !parse_array(sa, samp)) {
+            st = fail(TUNER_EINVAL, std::string("malformed trial-log line ") + std::to_string(lineno) + " in " + path);
+            break;
+        }
+        if (std::strncmp(k, key.c_str(), key.size()) != 0 || k[key.size()] != '"') continue;  // another problem
+        const int32_t sketch = (int32_t)std::strtol(sk, nullptr, 10);
+        int pos = -1;
+        for (size_t i = 0; i < spaces.size(); ++i)
+            if (spaces[i].sketch == sketch) pos = (int)i;
+        if (pos < 0 || (int)vals.size() != spaces[pos].nknobs()) continue;  // a sketch this tuner does not search
+        Pt p;
+        p.pos = pos;
+        p.n = spaces[pos].nknobs();
+        bool ok = true;
+        for (int d = 0; d < p.n && ok; ++d) {
+            const auto& vl = spaces[pos].values[d];
+            auto it = std::find(vl.begin(), vl.end(), (int32_t)vals[d]);
+            ok = it != vl.end();
+            if (ok) p.idx[d] = (int32_t)(it - vl.begin());
+        }
+        if (!ok || measured(p)) continue;
+        tuner_result smp;
+        std::memset(&smp, 0, sizeof(smp));
+        smp.pt = to_public(p);
+        smp.cost_ns = std::strncmp(co, "null", 4) == 0 ? INFINITY : std::strtod(co, nullptr);
+        smp.max_err = std::strtod(me, nullptr);
+        smp.status = (int32_t)std::strtol(ss, nullptr, 10);
+        smp.rank = (int32_t)std::strtol(rk, nullptr, 10);
+        if (smp.status != TUNER_S_OK) smp.cost_ns = INFINITY;
+        std::vector<float> fs(samp.begin(), samp.end());
+        if (fs.size() > (size_t)kMaxSamples) fs.resize(kMaxSamples);
+        record(p, smp, std::move(fs), false);
+        stats.replayed++;
+    }
+    std::fclose(f);
+    return st;
 }
 
 // ---------------------------------------------------------------- sampler (R-S1)
@@ -345,6 +535,7 @@ tuner_status Tuner::droplet(const Pt& start, int32_t budget, std::vector<Pt>& tr
     std::vector<Pt> nb, q, ray;
     int r = 1;  // ring radius (RADIUS policy, R-D16)
     for (;;) {
+        NvtxRange nv("droplet_round");
         ring(x, nb, r);
         if (r > 1 && nb.empty()) return finish(true);  // every axis line of x examined
         bool trunc = fresh(nb, q);
@@ -413,7 +604,7 @@ struct TableMeasurer : Measurer {
     std::vector<float> samples;  // optional [point][nsamp] repeat timings
     int nsamp = 0;
     TableMeasurer(Tuner* tt, std::vector<double>&& tab) : t(tt), table(std::move(tab)) {}
-    tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out, double) override {
+    tuner_status measure(const std::vector<Pt>& pts, std::vector<Result>& out, double, bool) override {
         out.assign(pts.size(), Result{});
         for (size_t i = 0; i < pts.size(); ++i) {
             const uint64_t id = t->linear(pts[i]);
@@ -555,6 +746,7 @@ extern "C" tuner_status tuner_create(int32_t op, const tuner_shape* shape, const
     }
     t->total = off;
     t->rng = SplitMix64(opts->seed);
+    t->key = problem_key(op, *shape);
     // the exchange step (R-M1): a caller-supplied host all-gather, or NCCL from a unique
     // id; an exchange given at world 1 is used too (one rank gathers its own slots)
     if (opts->allgather) {
@@ -577,6 +769,13 @@ extern "C" tuner_status tuner_create(int32_t op, const tuner_shape* shape, const
         tuner_status st = make_gpu_measurer(t.get(), t->measurer);
         if (st != TUNER_OK) return st;
     }
+    if (opts->trial_log && opts->trial_log[0]) {  // resume from, then append to, the trial log
+        tuner_status st = t->replay_log(opts->trial_log);
+        if (st != TUNER_OK) return st;
+        if (t->opts.rank == 0 && !(t->trial_log = std::fopen(opts->trial_log, "a")))
+            return fail(TUNER_EINVAL, std::string("cannot open trial log ") + opts->trial_log);
+    }
+    t->opts.trial_log = nullptr;  // borrowed for the call only
     *out = t.release();
     return TUNER_OK;
 }

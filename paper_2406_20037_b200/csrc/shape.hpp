@@ -57,6 +57,17 @@ inline size_t direct_smem_bytes(int rsc, int bkc, int px, int epi) {
     return wb > yb ? wb : yb;
 }
 
+// Stream-K workspace of the tcgen05 sketches (SCHED >= 1): `slots` flags (0 between launches:
+// heads re-arm their tails' flags) and one 128 x 256 fp32 partial tile per (group, CTA) slot.
+// Owned by a tuner handle and allocated outside graph capture; launches that share one
+// workspace must be ordered (one stream), launches of different handles never share one.
+struct StreamKScratch {
+    unsigned* flags = nullptr;
+    float* ws = nullptr;
+    int slots = 0;
+    int dev = -1;
+};
+
 struct ShapeInfo {  // derived GEMM view of the problem (depthwise: M = n*p*q, N = c, K = r*s)
     int32_t op, dtype;
     int64_t batch, M, N, K;     // GEMM: Y[batch][M][N] = A[batch][M][K] * B[batch][N][K]^T

@@ -16,7 +16,7 @@ static std::vector<SketchDesc> build_catalogue() {
     const std::vector<const char*> simt_names = {"BM", "BN", "BK", "TT", "UNROLL", "VEC", "STAGES", "SPLIT_K"};
     const std::vector<std::vector<int32_t>> simt_vals = {{16, 32, 64, 128}, {16, 32, 64, 128}, {4, 8, 16, 32},
                                                          {2, 4, 8},         {1, 2, 4, 8},       {1, 4},
-                                                         {1, 2},            {1, 2, 4, 8, 16}};
+                                                         {1, 2},            {1, 2, 3, 4, 6, 8, 12, 16}};
     c.push_back({SK_SIMT_GEMM_F32, "simt_gemm_f32", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL),
                  TUNER_F32, simt_names, simt_vals});
     c.push_back({SK_SIMT_IGEMM_CONV_F32, "simt_igemm_conv_f32", 1 << TUNER_OP_CONV2D, TUNER_F32, simt_names,
@@ -27,7 +27,7 @@ static std::vector<SketchDesc> build_catalogue() {
     const std::vector<const char*> pipe_names = {"BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K"};
     const std::vector<std::vector<int32_t>> pipe_vals = {{16, 32, 64, 128}, {32, 64, 128}, {8, 16, 32},
                                                          {2, 4},            {1, 2, 4},     {1, 4},
-                                                         {2, 3, 4, 6},      {1, 2, 4, 8, 16, 32}};
+                                                         {2, 3, 4, 6},      {1, 2, 3, 4, 6, 8, 12, 16, 24, 32}};
     c.push_back({SK_SIMT_PIPE_GEMM_F32, "simt_pipe_gemm_f32", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL),
                  TUNER_F32, pipe_names, pipe_vals});
     c.push_back({SK_SIMT_PIPE_CONV_F32, "simt_pipe_conv_f32", 1 << TUNER_OP_CONV2D, TUNER_F32, pipe_names,
@@ -58,7 +58,7 @@ static std::vector<SketchDesc> build_catalogue() {
     // 16-byte strides); a restricted compile-time lattice
     const std::vector<std::vector<int32_t>> simt16_vals = {{16, 32, 64, 128}, {16, 32, 64, 128}, {8, 16, 32},
                                                            {4, 8},            {1, 4},             {1, 4},
-                                                           {1, 2},            {1, 2, 4, 8, 16}};
+                                                           {1, 2},            {1, 2, 3, 4, 6, 8, 12, 16}};
     c.push_back({SK_SIMT_IGEMM_CONV_BF16, "simt_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, simt_names,
                  simt16_vals});
     // direct conv (SURVEY §8(d).1 `simt_direct_conv`) for few-input-channel layers: KT output
@@ -150,8 +150,11 @@ static bool simt_valid(const ShapeInfo& sh, const int32_t* v) {
     if (vec == 4 && (sh.op == TUNER_OP_CONV2D ? (sh.c % 4) : (sh.K % 4)) != 0) return false;
     const int64_t ktiles = (sh.K + bk - 1) / bk;
     if (split > ktiles) return false;  // empty K slices
+    if ((split - 1) * ((ktiles + split - 1) / split) >= ktiles) return false;  // a CTA slice would be empty
     const int64_t ntiles = (sh.N + bn - 1) / bn;
     if (ntiles > 65535 || (int64_t)split * sh.batch > 65535) return false;
+    // the conv gather keeps the image base offset n*H*W*C in 32-bit int
+    if (sh.op == TUNER_OP_CONV2D && sh.x_elems >= (1ll << 31)) return false;
     return true;
 }
 
@@ -166,11 +169,14 @@ static bool pipe_valid(const ShapeInfo& sh, const int32_t* v) {
     if ((chunks + threads - 1) / threads > kPipeMaxSlots) return false;  // cp.async slots per thread
     const int64_t ktiles = (sh.K + bk - 1) / bk;
     if (split > ktiles) return false;
+    if ((split - 1) * ((ktiles + split - 1) / split) >= ktiles) return false;  // a CTA slice would be empty
     const int64_t kspan = ((ktiles + split - 1) / split) * bk;
     if (pipe_smem_bytes(bm, bn, bk, kw, stages, conv, (int)kspan, vec, split) > 227 * 1024) return false;
     const int64_t ntiles = (sh.N + bn - 1) / bn;
     if (ntiles > 65535 || (int64_t)split * sh.batch > 65535) return false;
     if (conv && (sh.r - 1) * sh.dh >= 32767) return false;  // tap offsets packed in 16 bits
+    // the kernel forms element offsets (m * K, row * K, the conv image base) in 32-bit int
+    if (sh.x_elems >= (1ll << 31) || sh.w_elems >= (1ll << 31)) return false;
     return true;
 }
 

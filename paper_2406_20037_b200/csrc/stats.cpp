@@ -8,6 +8,8 @@
 #include <numeric>
 #include <vector>
 
+#include "internal.hpp"
+
 namespace db200 {
 
 double wilcoxon_p(const float* a, int n1, const float* b, int n2) {
@@ -46,3 +48,10 @@ double wilcoxon_p(const float* a, int n1, const float* b, int n2) {
 }
 
 }  // namespace db200
+
+extern "C" tuner_status tuner_rank_sum_p(const float* a, int32_t n1, const float* b, int32_t n2, double* p) {
+    if (!p || n1 < 0 || n2 < 0 || (n1 > 0 && !a) || (n2 > 0 && !b)) return db200::fail(TUNER_EINVAL, "bad arguments");
+    if (n1 > 16 || n2 > 16) return db200::fail(TUNER_EINVAL, "at most 16 samples per side (exact test)");
+    *p = db200::wilcoxon_p(a, n1, b, n2);
+    return TUNER_OK;
+}

@@ -99,6 +99,15 @@ def global_launch_count() -> int:
     return int(L.lib().tuner_global_launch_count())
 
 
+def rank_sum_p(a: Sequence[float], b: Sequence[float]) -> float:
+    """Two-sided exact Wilcoxon rank-sum p of two timing samples (tuner_rank_sum_p)."""
+    fa = (C.c_float * max(1, len(a)))(*a)
+    fb = (C.c_float * max(1, len(b)))(*b)
+    p = C.c_double()
+    L.check(L.lib().tuner_rank_sum_p(fa, len(a), fb, len(b), C.byref(p)))
+    return p.value
+
+
 def probe_fp32_peak(mode: int = 1) -> Tuple[float, float]:
     """FP32 pipe peak on the current device (tuner_probe_fp32_peak): (TFLOP/s, ms).
     mode 0 = 3-register FFMA, 1 = FFMA2, 2 = immediate-operand FFMA."""
@@ -137,7 +146,7 @@ class Tuner:
                  x=None, w=None, y=None, y_ref=None, y_absref=None, stream=None, group=None,
                  warmup: int = 2, repeats: int = 10, number: int = 0, max_batch: int = 512,
                  verify: bool = True, timeout_ms: float = 1000.0, early_cut: float = 0.0,
-                 alpha: float = 0.0, cost_samples=None):
+                 alpha: float = 0.0, cost_samples=None, trial_log: Optional[str] = None):
         lib = L.lib()
         self._h = C.c_void_p()
         self.op = op
@@ -160,6 +169,9 @@ class Tuner:
         o.timeout_ms, o.seed, o.policy = timeout_ms, seed, L.POLICY[policy]
         o.max_batch, o.verify, o.early_cut = max_batch, int(bool(verify)), float(early_cut)
         o.alpha = float(alpha)
+        if trial_log:
+            self._log = str(trial_log).encode()
+            o.trial_log = self._log
         if cost_table is not None:
             import numpy as np
             tab = np.ascontiguousarray(cost_table, dtype=np.float64)
@@ -299,7 +311,8 @@ class Tuner:
         s = L.Stats()
         L.check(L.lib().tuner_get_stats(self._h, C.byref(s)))
         return {"kernel_launches": s.kernel_launches, "candidates": s.candidates, "collectives": s.collectives,
-                "batches": s.batches, "measure_wall_ns": s.measure_wall_ns}
+                "batches": s.batches, "measure_wall_ns": s.measure_wall_ns, "early_cut": s.early_cut,
+                "light": s.light, "precise": s.precise, "calibrations": s.calibrations, "replayed": s.replayed}
 
     def values(self, p: PointT) -> List[int]:
         sid, idx = p

@@ -48,7 +48,7 @@ def test_catalogue():
     assert sketch_name(0) == "simt_gemm_f32"
     assert knob_names(0) == ["BM", "BN", "BK", "TT", "UNROLL", "VEC", "STAGES", "SPLIT_K"]
     sp = sketch_space(0)
-    assert sp[0] == [16, 32, 64, 128] and sp[7] == [1, 2, 4, 8, 16]
+    assert sp[0] == [16, 32, 64, 128] and sp[7] == [1, 2, 3, 4, 6, 8, 12, 16]
     assert knob_names(2) == ["BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER"]
     assert knob_names(3) == ["BM", "BN", "BK", "STAGES", "SPLIT_K", "TILE_Q", "SCHED", "RASTER"]
     assert sketch_name(8) == "simt_pipe_conv_f32"

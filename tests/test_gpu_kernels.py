@@ -217,34 +217,6 @@ def test_harness_sample_droplet_and_replay(policy):
     assert on.max_rel_err(y.cpu().numpy(), yo, ao) <= 1e-4
 
 
-def test_config1_bruteforce_and_droplet():
-    # BASELINE config 1: dense 512^3 fp32, 4-knob space (TT=4, SPLIT_K=1), 256 points, all valid
-    m = n = k = 512
-    x, w, yo, ao = gemm_case(1, m, n, k, "uniform", 0)
-    xd, wd = to_dev(x, w)
-    y = torch.empty(m, n, device=dev())
-    space = [[16, 32, 64, 128], [16, 32, 64, 128], [4, 8, 16, 32], [4], [1, 2, 4, 8], [4], [2], [1]]
-    import itertools
-    pts = [(0, idx) for idx in itertools.product(*[range(len(v)) for v in space])]
-    t = Tuner("dense", {"m": m, "n": n, "k": k}, spaces=[(0, space)], x=xd, w=wd, y=y, policy="grow")
-    assert all(t.valid(p) for p in pts) and len(pts) == 256
-    rep = t.droplet((0, (0,) * 8), 100)
-    res = t.measure(pts)
-    assert all(r.status == "ok" for r in res)
-    cost = {r.point: r.cost_ns for r in res}
-    best_bf = min(cost.values())
-    # converged => local minimum under the paper's neighbourhood (measured costs)
-    if rep["converged"]:
-        sp_ring = []
-        for d in range(8):
-            for dlt in (-1, 1):
-                i = rep["best"][1][d] + dlt
-                if 0 <= i < len(space[d]):
-                    q = list(rep["best"][1]); q[d] = i; sp_ring.append((0, tuple(q)))
-        assert all(cost[q] >= rep["best_cost"] for q in sp_ring)
-    print(f"config1: droplet {rep['best_cost']:.0f} ns in {rep['trials_used']} trials; brute force {best_bf:.0f} ns")
-
-
 # ---------------------------------------------------------------- tcgen05 bf16 sketch
 def bf16_case(b, m, n, k, dist, seed):
     x, w = tensors([(b, m, k), (b, n, k)], seed, dist)
@@ -296,14 +268,15 @@ def test_tc_harness_bert_like():
 
 
 @pytest.mark.parametrize("shape,vals", [
-    ((1, 75, 53, 36), [16, 16, 4, 2, 1, 1, 1, 8]),      # 9 k-tiles, 8 splits of 2: 5 take part
-    ((3, 33, 17, 130), [32, 16, 32, 2, 2, 1, 2, 4]),    # 5 k-tiles, 4 splits of 2: 3 take part
+    ((1, 75, 53, 36), [16, 16, 4, 2, 1, 1, 1, 2]),      # 9 k-tiles in 2 ragged slices (5 + 4)
+    ((3, 33, 17, 130), [32, 16, 32, 2, 2, 1, 2, 3]),    # 5 k-tiles in 3 ragged slices (2 + 2 + 1)
     ((1, 128, 128, 64), [64, 64, 16, 4, 4, 4, 2, 4]),
 ])
 def test_simt_split_k_repeat_and_graph(shape, vals):
     """Split-K (zeroing + atomic partial sums): back-to-back launches on the same y,
-    launches inside a captured CUDA graph, ragged k splits (CTAs with an empty k
-    range) -- every launch and every replay equals the oracle."""
+    launches inside a captured CUDA graph, ragged k splits (a shorter last slice; a split
+    that would leave a slice empty is statically invalid) -- every launch and every replay
+    equals the oracle."""
     b, m, n, k = shape
     op = "dense" if b == 1 else "batch_matmul"
     x, w, yo, ao = gemm_case(b, m, n, k, "uniform", 7 + k)
@@ -388,7 +361,8 @@ def test_nccl_exchange_path_world1():
         smp = t.sample(40)
         rep = t.droplet(t.best().point, 20)
         st = t.stats()
-        assert st["collectives"] >= 3 + rep["rounds"] - 1
+        # one all-gather per non-empty batch (world 1: no tier or calibration collectives)
+        assert st["collectives"] == st["batches"] >= 3 + 1
         assert len(smp) == 40 and all(s.status == "ok" and s.rank == 0 for s in smp)
         assert all(np.isfinite(s.cost_ns) for s in t.history())
         t.run(rep["best"], xd, wd, y)
