@@ -24,6 +24,7 @@ struct LaunchCtx {
     int dims[3] = {1, 1, 1};  // runtime thread-block shape knobs (depthwise: CT, QT, PT)
     int raster = 0;           // runtime tile order (tcgen05): 0 = M fastest, 1 = N fastest
     const StreamKScratch* sk = nullptr;  // stream-K workspace of the launching handle (SCHED >= 1)
+    int occ = 0;                         // runtime OCC knob (SIMT pipe): 0 = a CTA per unit, k = k CTAs/SM persistent
 };
 
 typedef cudaError_t (*LaunchFn)(const LaunchCtx&);

@@ -36,6 +36,10 @@ struct PipeParams {
     int H, W, Cin, P, Q, S, sh, sw, ph, pw, dh, dw;
     int vw;      // VEC knob: elements per cp.async (4 or 1)
     int stages;  // STAGES knob
+    // work units: (k slice, m tile, n tile, batch), k slice fastest; a CTA takes units
+    // blockIdx.x, + gridDim.x, ... (one unit per CTA when OCC = 0, persistent otherwise)
+    int units, m_tiles, n_tiles;
+    int persist;  // 1: the k table covers all of K and the epilogue tile has its own smem
 };
 
 constexpr bool pipe_static_ok(int BM, int BN, int BK, int TT, int KW) {
@@ -83,53 +87,44 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
     const size_t pipe_floats = (size_t)stages * STAGE_FLOATS;
     const bool staged_epi = KW > 1 || p.split > 1;  // epilogue through shared memory
     const size_t red_floats = staged_epi ? (size_t)KW * BM * BN : 0;
-    int2* ktab = reinterpret_cast<int2*>(smem + (pipe_floats > red_floats ? pipe_floats : red_floats));
+    // one-unit CTAs stage the epilogue tile over the drained ring; persistent CTAs keep the
+    // next unit's tiles in flight during an epilogue, so their tile has its own region
+    float* red = p.persist ? smem + pipe_floats : smem;
+    const size_t head = p.persist ? pipe_floats + red_floats : (pipe_floats > red_floats ? pipe_floats : red_floats);
+    int2* ktab = reinterpret_cast<int2*>(smem + head);
 
     const int tid = threadIdx.x;
     const int g = tid / GT, gt = tid % GT;
     const int tx = gt % TX, ty = gt / TX;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-    const int bz = blockIdx.z / p.split, kz = blockIdx.z % p.split;
-    const int kt_begin = kz * p.kt_per_split;
-    const int kt_end = min(p.ktiles, kt_begin + p.kt_per_split);
-    if (kt_begin >= kt_end) return;
-    const int nk = kt_end - kt_begin;
     constexpr int CPR = BK / VW;  // cp.async chunks per tile row
-    const int kbeg = kt_begin * BK;
+    const int u0 = blockIdx.x, ustep = gridDim.x;
+    if (u0 >= p.units) return;
 
-    const float* __restrict__ A = p.A + (CONV ? 0 : bz * p.sA);
-    const float* __restrict__ B = p.B + bz * p.sB;
-    float* __restrict__ C = p.C + bz * p.sC;
+    // unit -> (k slice, m tile, n tile, batch), k slice fastest
+    struct Unit {
+        int m0, n0, bz, kt_begin, nk;
+    };
+    auto unit_of = [&](int u) {
+        Unit w;
+        const int kz = u % p.split;
+        int t = u / p.split;
+        w.m0 = (t % p.m_tiles) * BM;
+        t /= p.m_tiles;
+        w.n0 = (t % p.n_tiles) * BN;
+        w.bz = t / p.n_tiles;
+        w.kt_begin = kz * p.kt_per_split;
+        w.nk = min(p.ktiles, w.kt_begin + p.kt_per_split) - w.kt_begin;  // >= 1 (static validity)
+        return w;
+    };
 
-    // per-slot fixed state: a slot is (row, k chunk) of the tile, the same for every k-tile
-    constexpr int chunksA = BM * CPR, chunksB = BN * CPR;
-    constexpr int SA = (chunksA + NT - 1) / NT, SB = (chunksB + NT - 1) / NT;  // slots per thread
-    static_assert(SA <= kPipeMaxSlots && SB <= kPipeMaxSlots, "slot budget (static validity rule)");
-    // A slots: image / row base, h0, w0 (conv) or row offset (dense; h0 = 0 marks a valid row)
-    int abase[SA], ah0[SA], aw0[SA];
-#pragma unroll
-    for (int i = 0; i < SA; ++i) {
-        const int e = tid + i * NT;
-        const int row = e / CPR;
-        int base = 0, h0 = -(1 << 29), w0 = 0;
-        if (e < chunksA && m0 + row < p.M) {
-            const int m = m0 + row;
-            if constexpr (CONV) {
-                const int q = m % p.Q, t = m / p.Q, pp = t % p.P, n = t / p.P;
-                h0 = pp * p.sh - p.ph;
-                w0 = q * p.sw - p.pw;
-                base = n * p.H * p.W * p.Cin + (h0 * p.W + w0) * p.Cin;
-            } else {
-                base = m * p.K;
-                h0 = 0;
-            }
-        }
-        abase[i] = base; ah0[i] = h0; aw0[i] = w0;
-    }
-    if constexpr (CONV) {  // koff / tap offsets of every reduction chunk in this CTA's k range
-        const int nent = (nk * BK) / VW;
+    // the conv k table: koff / tap offsets of every reduction chunk, for the CTA's k range
+    // (one unit) or for all of K (persistent: units of every k slice)
+    const Unit first = unit_of(u0);
+    const int ktab_k0 = p.persist ? 0 : first.kt_begin * BK;
+    if constexpr (CONV) {
+        const int nent = p.persist ? (p.ktiles * BK) / VW : (first.nk * BK) / VW;
         for (int j = tid; j < nent; j += NT) {
-            const int kk = kbeg + j * VW;
+            const int kk = ktab_k0 + j * VW;
             int2 t = make_int2(0, 0x7FFF7FFF);  // out of range: fails the image bounds check
             if (kk < p.K) {
                 const int rs = kk / p.Cin, c = kk - rs * p.Cin, r = rs / p.S, s = rs - r * p.S;
@@ -141,19 +136,51 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
         __syncthreads();
     }
 
-    // B slots: element offset of the slot's first k in this CTA's range (-1: row outside N)
-    int boff[SB];
+    // per-slot producer state of the unit being loaded: a slot is (row, k chunk) of the tile,
+    // the same for every k-tile of a unit
+    constexpr int chunksA = BM * CPR, chunksB = BN * CPR;
+    constexpr int SA = (chunksA + NT - 1) / NT, SB = (chunksB + NT - 1) / NT;  // slots per thread
+    static_assert(SA <= kPipeMaxSlots && SB <= kPipeMaxSlots, "slot budget (static validity rule)");
+    int abase[SA], ah0[SA], aw0[SA];  // A: image / row base, h0, w0 (conv) or row offset (dense; h0 = 0 = valid)
+    int boff[SB];                     // B: element offset of the row (-1: row outside N)
+    const float* Ab = p.A;
+    const float* Bb = p.B;
+    Unit lw = first;  // the unit the producer is loading
+    auto set_unit = [&](const Unit& w) {
+        Ab = p.A + (CONV ? 0 : w.bz * p.sA);
+        Bb = p.B + w.bz * p.sB;
 #pragma unroll
-    for (int i = 0; i < SB; ++i) {
-        const int e = tid + i * NT, row = e / CPR, kl = (e % CPR) * VW;
-        boff[i] = (e < chunksB && n0 + row < p.N) ? (n0 + row) * p.K + kbeg + kl : -1;
-    }
+        for (int i = 0; i < SA; ++i) {
+            const int e = tid + i * NT;
+            const int row = e / CPR;
+            int base = 0, h0 = -(1 << 29), w0 = 0;
+            if (e < chunksA && w.m0 + row < p.M) {
+                const int m = w.m0 + row;
+                if constexpr (CONV) {
+                    const int q = m % p.Q, t = m / p.Q, pp = t % p.P, n = t / p.P;
+                    h0 = pp * p.sh - p.ph;
+                    w0 = q * p.sw - p.pw;
+                    base = n * p.H * p.W * p.Cin + (h0 * p.W + w0) * p.Cin;
+                } else {
+                    base = m * p.K;
+                    h0 = 0;
+                }
+            }
+            abase[i] = base; ah0[i] = h0; aw0[i] = w0;
+        }
+#pragma unroll
+        for (int i = 0; i < SB; ++i) {
+            const int e = tid + i * NT, row = e / CPR;
+            boff[i] = (e < chunksB && w.n0 + row < p.N) ? (w.n0 + row) * p.K : -1;
+        }
+    };
+    set_unit(lw);
 
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
-    auto load_tile = [&](int stage, int kt) {  // kt relative to kt_begin
+    auto load_tile = [&](int stage, int kt) {  // kt relative to the loaded unit's first k-tile
         const uint32_t as = ring_s + (uint32_t)(stage * STAGE_FLOATS) * 4u;
         const uint32_t bs = as + (uint32_t)(BM * LDK) * 4u;
-        const int k0 = kt * BK;  // local k offset
+        const int kb = (lw.kt_begin + kt) * BK;  // absolute k of the tile
 #pragma unroll
         for (int i = 0; i < SA; ++i) {
             const int e = tid + i * NT;
@@ -163,16 +190,16 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
                 // branch-free: an out-of-image tap copies 0 bytes from the tensor base
                 int ok, off;
                 if constexpr (CONV) {
-                    const int2 t = ktab[(k0 + kl) / VW];
+                    const int2 t = ktab[(kb - ktab_k0 + kl) / VW];
                     const int h = ah0[i] + (t.y >> 16), w = aw0[i] + (t.y & 0xFFFF);
                     ok = (unsigned)h < (unsigned)p.H && (unsigned)w < (unsigned)p.W;
                     off = ok ? abase[i] + t.x : 0;
                 } else {
-                    const int kk = kbeg + k0 + kl;
+                    const int kk = kb + kl;
                     ok = ah0[i] == 0 && kk < p.K;
                     off = ok ? abase[i] + kk : 0;
                 }
-                const float* src = A + off;
+                const float* src = Ab + off;
                 if constexpr (VW == 4) cp_async16(dst, src, ok ? 16 : 0);
                 else cp_async4(dst, src, ok ? 4 : 0);
             }
@@ -183,8 +210,8 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
             if (chunksB % NT == 0 || e < chunksB) {
                 const int row = e / CPR, kl = (e % CPR) * VW;
                 const uint32_t dst = bs + (uint32_t)(row * LDK + kl) * 4u;
-                const bool ok = boff[i] >= 0 && kbeg + k0 + kl < p.K;
-                const float* src = B + (ok ? boff[i] + k0 : 0);
+                const bool ok = boff[i] >= 0 && kb + kl < p.K;
+                const float* src = Bb + (ok ? boff[i] + kb + kl : 0);
                 if constexpr (VW == 4) cp_async16(dst, src, ok ? 16 : 0);
                 else cp_async4(dst, src, ok ? 4 : 0);
             }
@@ -236,46 +263,29 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
         }
     };
 
-    // multistage ring: STAGES-1 tiles in flight while one is consumed
-    for (int s = 0; s < stages - 1; ++s) {
-        if (s < nk) load_tile(s, s);
-        cp_commit();
-    }
-    int cs = 0, ls = stages - 1;  // stage consumed / stage refilled this iteration (no modulo)
-    for (int it = 0; it < nk; ++it) {
-        cp_wait_stages(stages);
-        __syncthreads();  // tile `it` visible to all; every thread is done with tile it-1's stage
-        const int nxt = it + stages - 1;
-        if (nxt < nk) load_tile(ls, nxt);
-        cp_commit();
-        compute(cs);
-        cs = cs + 1 == stages ? 0 : cs + 1;
-        ls = ls + 1 == stages ? 0 : ls + 1;
-    }
-
     const bool atomic = p.split > 1;
-    if (atomic) griddep_wait();  // Y zeroed by the prerequisite grid (PDL)
-    if (!staged_epi) {  // KW = 1, no split-K: direct stores from the accumulators
+    // epilogue of the unit `w` the consumer just finished: its accumulators -> Y
+    auto epilogue = [&](const Unit& w) {
+        float* __restrict__ C = p.C + w.bz * p.sC;
+        if (atomic) griddep_wait();  // Y zeroed by the prerequisite grid (PDL); returns at once later
+        if (!staged_epi) {  // KW = 1, no split-K: direct stores from the accumulators
 #pragma unroll
-        for (int i = 0; i < TT; ++i) {
-            const int m = m0 + ty + i * TY;
-            if (m >= p.M) continue;
-            float* crow = C + (long long)m * p.N;
+            for (int i = 0; i < TT; ++i) {
+                const int m = w.m0 + ty + i * TY;
+                if (m >= p.M) continue;
+                float* crow = C + (long long)m * p.N;
 #pragma unroll
-            for (int j = 0; j < TT; ++j) {
-                const int n = n0 + tx + j * TX;
-                if (n < p.N) {
-                    const float v = acc[i][j].x + acc[i][j].y;
-                    if (atomic) atomicAdd(crow + n, v);
-                    else crow[n] = v;
+                for (int j = 0; j < TT; ++j) {
+                    const int n = w.n0 + tx + j * TX;
+                    if (n < p.N) crow[n] = acc[i][j].x + acc[i][j].y;
                 }
             }
+            return;
         }
-    } else {  // the KW groups' partial tiles summed through shared memory; 128-bit stores or
-              // (split-K) 128-bit atomics from the staged tile
-        cp_wait<0>();
-        __syncthreads();
-        float* red = smem;  // [KW][BM][BN]
+        // the KW groups' partial tiles summed through shared memory; 128-bit stores or
+        // (split-K) 128-bit atomics from the staged tile
+        if (!p.persist) cp_wait<0>();  // the tile overlaps the (drained) ring
+        __syncthreads();               // every thread is done reading the previous staged tile
 #pragma unroll
         for (int i = 0; i < TT; ++i)
 #pragma unroll
@@ -285,7 +295,7 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
         const bool vec_ok = (p.N % 4) == 0;
         for (int e = tid; e < BM * BN / 4; e += NT) {
             const int row = e / (BN / 4), col = (e % (BN / 4)) * 4;
-            const int m = m0 + row, n = n0 + col;
+            const int m = w.m0 + row, n = w.n0 + col;
             if (m >= p.M) continue;
             float4 v = *reinterpret_cast<const float4*>(red + row * BN + col);
 #pragma unroll
@@ -306,6 +316,49 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
                         else cp[q] = vv[q];
                     }
             }
+        }
+    };
+
+    // multistage ring over the concatenated k-tiles of this CTA's units: STAGES-1 tiles in
+    // flight while one is consumed; a persistent CTA's producer runs into the next unit's
+    // tiles while the consumer finishes the current one (no pipeline drain between units)
+    int lu = u0, lkt = 0;  // producer cursor: unit, k-tile within it
+    auto produce = [&](int stage) {
+        if (lu >= p.units) return;
+        load_tile(stage, lkt);
+        if (++lkt == lw.nk) {
+            lkt = 0;
+            lu += ustep;
+            if (lu < p.units) {
+                lw = unit_of(lu);
+                set_unit(lw);
+            }
+        }
+    };
+    for (int s = 0; s < stages - 1; ++s) {
+        produce(s);
+        cp_commit();
+    }
+    Unit cw = first;  // the unit the consumer is computing
+    int ckt = 0;
+    int cs = 0, ls = stages - 1;  // stage consumed / stage refilled this iteration (no modulo)
+    for (int cu = u0; cu < p.units;) {
+        cp_wait_stages(stages);
+        __syncthreads();  // tile visible to all; every thread is done with the previous tile's stage
+        produce(ls);
+        cp_commit();
+        compute(cs);
+        cs = cs + 1 == stages ? 0 : cs + 1;
+        ls = ls + 1 == stages ? 0 : ls + 1;
+        if (++ckt == cw.nk) {
+            epilogue(cw);
+#pragma unroll
+            for (int i = 0; i < TT; ++i)
+#pragma unroll
+                for (int j = 0; j < TT; ++j) acc[i][j] = make_float2(0.f, 0.f);
+            ckt = 0;
+            cu += ustep;
+            if (cu < p.units) cw = unit_of(cu);
         }
     }
 }
@@ -333,13 +386,26 @@ cudaError_t pipe_launch(const LaunchCtx& c) {
     p.sh = s.sh; p.sw = s.sw; p.ph = s.ph; p.pw = s.pw; p.dh = s.dh; p.dw = s.dw;
     p.vw = VW;
     p.stages = c.stages;
+    p.m_tiles = (int)((s.M + BM - 1) / BM);
+    p.n_tiles = (int)((s.N + BN - 1) / BN);
+    const long long units = (long long)p.m_tiles * p.n_tiles * s.batch * c.split;
+    if (units >= (1ll << 31)) return cudaErrorInvalidValue;
+    p.units = (int)units;
+    // OCC knob: 0 = one CTA per unit; k > 0 = persistent, k CTAs per SM walking the units
+    long long grid = units;
+    p.persist = 0;
+    if (c.occ > 0 && units > (long long)c.occ * c.num_sms) {
+        grid = (long long)c.occ * c.num_sms;
+        p.persist = 1;
+    }
     if (c.split > 1) {
         cudaError_t e = zero_for_splitk((float*)c.y, s.y_elems, c.stream);
         if (e != cudaSuccess) return e;
     }
-    const size_t smem = pipe_smem_bytes(BM, BN, BK, KW, p.stages, CONV, p.kt_per_split * BK, p.vw, p.split);
+    const size_t smem = pipe_smem_bytes(BM, BN, BK, KW, p.stages, CONV, p.persist ? p.ktiles * BK : p.kt_per_split * BK,
+                                        p.vw, p.split, p.persist);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)((s.M + BM - 1) / BM), (unsigned)((s.N + BN - 1) / BN), (unsigned)(s.batch * c.split));
+    cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;

@@ -38,13 +38,15 @@ constexpr bool dw_win_fits(int vec, int tq, int tp, int ks, int sh) {
 // cp.async multistage SIMT sketches: shared-memory bytes of a launch (ring of STAGES
 // [BM+BN][BK+4] fp32 tiles, or the reduction tile if larger -- KW group partials, or the
 // split-K tile staged for 128-bit atomics -- + the conv k table)
+// (persistent CTAs: ring + reduction tile side by side, the k table over all of K)
 inline size_t pipe_smem_bytes(int bm, int bn, int bk, int kw, int stages, bool conv, int kspan, int vw,
-                              int split) {
+                              int split, int persist = 0) {
     const size_t pipe = (size_t)stages * (bm + bn) * (bk + 4) * 4;
     const size_t red = (kw > 1 || split > 1) ? (size_t)kw * bm * bn * 4 : 0;
     const size_t ktab = conv ? (size_t)((kspan + vw - 1) / vw) * 8 : 0;
-    return (pipe > red ? pipe : red) + ktab;
+    return (persist ? pipe + red : (pipe > red ? pipe : red)) + ktab;
 }
+constexpr int kB200Sms = 148;  // static validity rules that depend on the SM count (B200 only)
 constexpr int kPipeMaxSlots = 8;  // cp.async slots per thread per operand
 
 // direct conv sketches: the block-size bound of an instantiation (its accumulators need

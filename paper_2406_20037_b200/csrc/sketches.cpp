@@ -24,10 +24,13 @@ static std::vector<SketchDesc> build_catalogue() {
     // cp.async multistage SIMT fp32 family (kernels/simt_pipe.cuh): STAGES-deep cp.async
     // ring with zero-fill gathers, KW warp groups slicing each staged k-tile (summed through
     // shared memory), k-parity FFMA2 accumulators; VEC = cp.async width, SPLIT_K as above.
-    const std::vector<const char*> pipe_names = {"BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K"};
+    // OCC (runtime): 0 = one CTA per work unit (tile x k slice); k > 0 = k persistent CTAs per
+    // SM walking the units, the cp.async ring running on into the next unit's tiles.
+    const std::vector<const char*> pipe_names = {"BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K", "OCC"};
     const std::vector<std::vector<int32_t>> pipe_vals = {{16, 32, 64, 128}, {32, 64, 128}, {8, 16, 32},
                                                          {2, 4},            {1, 2, 4},     {1, 4},
-                                                         {2, 3, 4, 6},      {1, 2, 3, 4, 6, 8, 12, 16, 24, 32}};
+                                                         {2, 3, 4, 6},      {1, 2, 3, 4, 6, 8, 12, 16, 24, 32},
+                                                         {0, 1, 2, 3, 4}};
     c.push_back({SK_SIMT_PIPE_GEMM_F32, "simt_pipe_gemm_f32", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL),
                  TUNER_F32, pipe_names, pipe_vals});
     c.push_back({SK_SIMT_PIPE_CONV_F32, "simt_pipe_conv_f32", 1 << TUNER_OP_CONV2D, TUNER_F32, pipe_names,
@@ -159,7 +162,8 @@ static bool simt_valid(const ShapeInfo& sh, const int32_t* v) {
 }
 
 static bool pipe_valid(const ShapeInfo& sh, const int32_t* v) {
-    const int bm = v[0], bn = v[1], bk = v[2], tt = v[3], kw = v[4], vec = v[5], stages = v[6], split = v[7];
+    const int bm = v[0], bn = v[1], bk = v[2], tt = v[3], kw = v[4], vec = v[5], stages = v[6], split = v[7],
+              occ = v[8];
     const bool conv = sh.op == TUNER_OP_CONV2D;
     if (tt > bm || tt > bn) return false;
     const int gt = (bm / tt) * (bn / tt), threads = gt * kw;
@@ -172,6 +176,12 @@ static bool pipe_valid(const ShapeInfo& sh, const int32_t* v) {
     if ((split - 1) * ((ktiles + split - 1) / split) >= ktiles) return false;  // a CTA slice would be empty
     const int64_t kspan = ((ktiles + split - 1) / split) * bk;
     if (pipe_smem_bytes(bm, bn, bk, kw, stages, conv, (int)kspan, vec, split) > 227 * 1024) return false;
+    if (occ > 0) {  // persistent: only when there are more units than CTAs (else = OCC 0)
+        const int64_t units = ((sh.M + bm - 1) / bm) * ((sh.N + bn - 1) / bn) * sh.batch * split;
+        if (units <= (int64_t)occ * kB200Sms) return false;
+        if (pipe_smem_bytes(bm, bn, bk, kw, stages, conv, (int)(ktiles * bk), vec, split, 1) > 227 * 1024)
+            return false;
+    }
     const int64_t ntiles = (sh.N + bn - 1) / bn;
     if (ntiles > 65535 || (int64_t)split * sh.batch > 65535) return false;
     if (conv && (sh.r - 1) * sh.dh >= 32767) return false;  // tap offsets packed in 16 bits

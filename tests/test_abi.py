@@ -52,7 +52,7 @@ def test_catalogue():
     assert knob_names(2) == ["BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER"]
     assert knob_names(3) == ["BM", "BN", "BK", "STAGES", "SPLIT_K", "TILE_Q", "SCHED", "RASTER"]
     assert sketch_name(8) == "simt_pipe_conv_f32"
-    assert knob_names(8) == ["BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K"]
+    assert knob_names(8) == ["BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K", "OCC"]
     assert sketch_name(10) == "simt_direct_conv_bf16"
     assert knob_names(9) == ["KT", "TP", "PX", "BKC", "EPI"]
     assert sketch_name(99) is None
@@ -65,3 +65,12 @@ def test_measured_mode_rejects_uncompiled_values():
     with pytest.raises(TunerError, match="EINVAL"):
         Tuner("dense", {"m": 4, "n": 4, "k": 4}, spaces=[(0, [[24], [16], [4], [4], [1], [4], [2], [1]])], x=x, w=x, y=x,
               stream=0)
+
+
+def test_instantiation_lists_match_their_generator():
+    # the explicit-instantiation TUs of the SIMT sketches are exactly what tools/gen_instantiations.py emits
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gen_instantiations.py"), "--check"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr

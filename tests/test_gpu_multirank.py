@@ -69,7 +69,8 @@ def test_measured_mode_world2_on_one_gpu(tmp_path):
     hist = r0["history"]
     assert r0["n_sample"] == 128
     assert {h[4] for h in hist} == {0, 1}, "both ranks measured candidates"
-    assert all(h[3] == 0 and h[5] <= 1e-4 for h in hist), "every candidate verified ok"
+    bad = [h for h in hist if not (h[3] == "ok" and h[5] <= 1e-4)]
+    assert not bad, ("every candidate verified ok", bad[:8])
     rank_of = {(h[0], tuple(h[1])): h[4] for h in hist}
     for p in r0["traj"]:
         assert rank_of[(p[0], tuple(p[1]))] == 0, ("accepted point not re-timed on rank 0", p)
