@@ -140,7 +140,7 @@ static tuner_status wait_progress(const std::vector<cudaEvent_t>& evs, double st
 
 // launcher + runtime knobs of a point
 struct RuntimeKnobs {
-    int split = 1, vec = 1, stages = 1, sched = 0, raster = 0, occ = 0;
+    int split = 1, vec = 1, stages = 1, sched = 0, raster = 0, occ = 0, red = 0, epi = 1;
     int dims[3] = {1, 1, 1};
 };
 static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
@@ -156,22 +156,25 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
             rk.stages = v[6];
             rk.split = v[7];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[4]));
-        case SK_SIMT_PIPE_GEMM_F32:  // BM, BN, BK, TT, KW, VEC (compiled) | STAGES, SPLIT_K, OCC
+        case SK_SIMT_PIPE_GEMM_F32:  // BM, BN, BK, TT, KW, VEC (compiled) | STAGES, SPLIT_K, OCC, RED
         case SK_SIMT_PIPE_CONV_F32:
             rk.vec = v[5];
             rk.stages = v[6];
             rk.split = v[7];
             rk.occ = v[8];
+            rk.red = v[9];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[4] | (v[5] << 4)));
-        case SK_TC_GEMM_BF16:  // BM, BN, BK, STAGES, SPLIT_K, SCHED, RASTER
+        case SK_TC_GEMM_BF16:  // BM, BN, BK, STAGES, SPLIT_K, SCHED, RASTER, EPI
             rk.split = v[4];
             rk.sched = v[5];
             rk.raster = v[6];
+            rk.epi = v[7];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], 0));
-        case SK_TC_IGEMM_CONV_BF16:  // BM, BN, BK, STAGES, SPLIT_K, TILE_Q, SCHED, RASTER
+        case SK_TC_IGEMM_CONV_BF16:  // BM, BN, BK, STAGES, SPLIT_K, TILE_Q, SCHED, RASTER, EPI
             rk.split = v[4];
             rk.sched = v[6];
             rk.raster = v[7];
+            rk.epi = v[8];
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[5]));
         case SK_SIMT_DIRECT_CONV_F32:  // KT, TP (compiled) | PX, BKC, EPI
         case SK_SIMT_DIRECT_CONV_BF16:
@@ -327,6 +330,8 @@ struct GpuMeasurer : Measurer {
         for (int d = 0; d < 3; ++d) b.ctx.dims[d] = b.rk[j].dims[d];
         b.ctx.raster = b.rk[j].raster;
         b.ctx.occ = b.rk[j].occ;
+        b.ctx.red = b.rk[j].red;
+        b.ctx.epi = b.rk[j].epi;
     }
 
     // nwin back-to-back windows of `num` launches of candidate j, bracketed by events
@@ -646,6 +651,8 @@ tuner_status gpu_kernel_run(Tuner* t, const Pt& p, const tuner_buffers* buf, voi
     for (int d = 0; d < 3; ++d) ctx.dims[d] = rk.dims[d];
     ctx.raster = rk.raster;
     ctx.occ = rk.occ;
+    ctx.red = rk.red;
+    ctx.epi = rk.epi;
     ctx.sk = &t->sk;
     CU(fn(ctx));
     return TUNER_OK;

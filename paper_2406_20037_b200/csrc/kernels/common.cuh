@@ -25,6 +25,8 @@ struct LaunchCtx {
     int raster = 0;           // runtime tile order (tcgen05): 0 = M fastest, 1 = N fastest
     const StreamKScratch* sk = nullptr;  // stream-K workspace of the launching handle (SCHED >= 1)
     int occ = 0;                         // runtime OCC knob (SIMT pipe): 0 = a CTA per unit, k = k CTAs/SM persistent
+    int red = 0;                         // runtime RED knob (SIMT pipe): split-K by 0 = atomics, 1 = cluster DSMEM
+    int epi = 1;                         // runtime EPI knob (tcgen05): epilogue staging buffer sets per warp
 };
 
 typedef cudaError_t (*LaunchFn)(const LaunchCtx&);

@@ -40,6 +40,8 @@ struct PipeParams {
     // blockIdx.x, + gridDim.x, ... (one unit per CTA when OCC = 0, persistent otherwise)
     int units, m_tiles, n_tiles;
     int persist;  // 1: the k table covers all of K and the epilogue tile has its own smem
+    int cred;     // 1: the SPLIT_K CTAs of a tile form a cluster and reduce their partial tiles
+                  //    through distributed shared memory (no zeroing kernel, no atomics)
 };
 
 constexpr bool pipe_static_ok(int BM, int BN, int BK, int TT, int KW) {
@@ -65,6 +67,10 @@ __device__ __forceinline__ void cp_wait_stages(int stages) {  // wait until <= S
         case 4: cp_wait<2>(); break;
         default: cp_wait<4>(); break;  // 6
     }
+}
+
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // (a.x*b.x + c.x, a.y*b.y + c.y): two RN fused multiply-adds in one FFMA2
@@ -263,9 +269,68 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
         }
     };
 
-    const bool atomic = p.split > 1;
+    const bool atomic = p.split > 1 && !p.cred;
+    // split-K inside a cluster (RED = 1): the split CTAs of a tile are one cluster; each stages
+    // its partial tile (KW groups summed) in shared memory, and after a cluster barrier CTA r
+    // sums rows [r*BM/S, (r+1)*BM/S) of all S partial tiles over distributed shared memory
+    // (ld.shared::cluster) and stores them -- Y written once, in order-independent of timing
+    auto epilogue_cluster = [&](const Unit& w) {
+        float* __restrict__ C = p.C + w.bz * p.sC;
+        cp_wait<0>();
+        __syncthreads();  // the ring is drained; the tile overlaps it
+#pragma unroll
+        for (int i = 0; i < TT; ++i)
+#pragma unroll
+            for (int j = 0; j < TT; ++j)
+                red[(g * BM + ty + i * TY) * BN + tx + j * TX] = acc[i][j].x + acc[i][j].y;
+        if constexpr (KW > 1) {
+            __syncthreads();
+            for (int e = tid; e < BM * BN / 4; e += NT) {
+                float4 v = reinterpret_cast<const float4*>(red)[e];
+#pragma unroll
+                for (int q = 1; q < KW; ++q) {
+                    const float4 u = reinterpret_cast<const float4*>(red + q * BM * BN)[e];
+                    v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+                }
+                reinterpret_cast<float4*>(red)[e] = v;
+            }
+        }
+        cluster_barrier();  // every CTA's partial tile is in its shared memory
+        const int S = p.split;
+        uint32_t rank;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        const int rp = (BM + S - 1) / S, r0 = (int)rank * rp, r1 = min(BM, r0 + rp);
+        const uint32_t red_s = (uint32_t)__cvta_generic_to_shared(red);
+        const bool vec_ok = (p.N % 4) == 0;
+        for (int e = r0 * (BN / 4) + tid; e < r1 * (BN / 4); e += NT) {
+            const int row = e / (BN / 4), col = (e % (BN / 4)) * 4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < S; ++q) {
+                uint32_t ra;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(red_s + (uint32_t)e * 16u), "r"(q));
+                float4 u;
+                asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(u.x), "=f"(u.y), "=f"(u.z), "=f"(u.w) : "r"(ra) : "memory");
+                v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+            }
+            const int m = w.m0 + row, n = w.n0 + col;
+            if (m >= p.M) continue;
+            float* cp = C + (long long)m * p.N + n;
+            if (vec_ok && n + 3 < p.N) {
+                *reinterpret_cast<float4*>(cp) = v;
+            } else {
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (n + q < p.N) cp[q] = vv[q];
+            }
+        }
+        cluster_barrier();  // no CTA leaves while its peers still read its shared memory
+    };
+
     // epilogue of the unit `w` the consumer just finished: its accumulators -> Y
     auto epilogue = [&](const Unit& w) {
+        if (p.cred) return epilogue_cluster(w);
         float* __restrict__ C = p.C + w.bz * p.sC;
         if (atomic) griddep_wait();  // Y zeroed by the prerequisite grid (PDL); returns at once later
         if (!staged_epi) {  // KW = 1, no split-K: direct stores from the accumulators
@@ -398,7 +463,11 @@ cudaError_t pipe_launch(const LaunchCtx& c) {
         grid = (long long)c.occ * c.num_sms;
         p.persist = 1;
     }
-    if (c.split > 1) {
+    // RED knob: 1 = split-K reduced inside a cluster of the tile's SPLIT_K CTAs (k slice
+    // fastest, so consecutive CTAs = one tile's slices = one cluster)
+    p.cred = (c.red == 1 && c.split > 1 && !p.persist) ? 1 : 0;
+    if (c.red == 1 && !p.cred) return cudaErrorInvalidConfiguration;
+    if (c.split > 1 && !p.cred) {
         cudaError_t e = zero_for_splitk((float*)c.y, s.y_elems, c.stream);
         if (e != cudaSuccess) return e;
     }
@@ -410,7 +479,14 @@ cudaError_t pipe_launch(const LaunchCtx& c) {
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];
-    if (c.split > 1) {  // launch early; the kernel waits for the zeroing before its atomics
+    if (p.cred) {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)c.split;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    } else if (c.split > 1) {  // launch early; the kernel waits for the zeroing before its atomics
         pdl_attr(attr[0]);
         cfg.attrs = attr;
         cfg.numAttrs = 1;

@@ -51,12 +51,16 @@ struct TcCfg {
     static constexpr int B_BYTES = BNC * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
-    // epilogue staging for TMA stores: per epilogue warp two 32-row x 16-column fp32
-    // boxes (double-buffered against the asynchronous bulk stores)
-    static constexpr int EPI_BOX = 32 * 16;
+    // epilogue staging for TMA stores: per epilogue warp one 64-column TMEM chunk = two
+    // 32-row x 32-column fp32 boxes whose 128-byte rows are stored 128B-swizzled (bank-conflict
+    // free st.shared.v4, and the layout the tensor map's SWIZZLE_128B expects), written with ONE
+    // proxy fence and two TMA stores per chunk; 1024-byte aligned, right after the stages
+    // (EPI knob: 1 or 2 such buffer sets; with 2 a warp writes chunk c while chunk c-1's stores
+    // still read the other set)
+    static constexpr int EPI_BOX = 32 * 32;
     static constexpr int EPI_BYTES = 4 * 2 * EPI_BOX * 4;
     static_assert(EPI_BYTES == kTcEpiBytes, "epilogue staging size");
-    static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256 + EPI_BYTES;
+    static constexpr size_t smem(int epi) { return 1024 + (size_t)STAGES * STAGE_BYTES + (size_t)epi * EPI_BYTES + 256; }
     static constexpr int THREADS = 192;
 };
 
@@ -68,6 +72,7 @@ struct TcParams {
     int units;                    // SCHED 0: batch * mp_tiles * n_tiles * split
     int sched;                    // 0 = tiles (+ split-K), 1 = stream-K, 2 = full waves by tile + k-chunked rest
     int raster;                   // tile order: 0 = M fastest, 1 = N fastest
+    int epi;                      // EPI knob: epilogue staging buffer sets per warp (1 or 2)
     int dp_tiles;                 // SCHED 2: tiles handled whole (a multiple of the group count)
     int rem_tiles, rem_chunks;    // SCHED 2: remainder tiles and k-chunks per remainder tile
     long long total_iters;        // SCHED 1/2: streamed k-block iterations (tiles - dp_tiles) * kblocks
@@ -198,13 +203,13 @@ __global__ void __launch_bounds__(192, 1)
     constexpr int TP = CONV ? BM / TQ : 1;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(base + STAGES * Cfg::STAGE_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + STAGES * Cfg::STAGE_BYTES + p.epi * Cfg::EPI_BYTES);
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
     uint64_t* acc_full = bars + 2 * STAGES;       // [2] MMA -> epilogue
     uint64_t* acc_empty = bars + 2 * STAGES + 2;  // [2] epilogue -> MMA
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
-    float* epi_smem = reinterpret_cast<float*>(base + STAGES * Cfg::STAGE_BYTES + 256);
+    float* epi_smem = reinterpret_cast<float*>(base + STAGES * Cfg::STAGE_BYTES);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? tc::cluster_ctarank() : 0u;
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(192, 1)
         const int q = warp & 3;
         const int trow = q * 32 + lane;  // row of the 128-row sub-tile held by this thread
         const bool vec_ok = (p.N % 4) == 0;  // TMA needs 16-byte global strides
-        int ebuf = 0;                        // staging boxes used so far by this warp
+        int ec = 0;                          // TMA-stored chunks so far (staging buffer = ec % EPI)
         int j = 0;
         SegIter si(p, group, ngroups);
         Seg w;
@@ -424,22 +429,36 @@ __global__ void __launch_bounds__(192, 1)
                             }
                     }
                 }
+                if (w.mode != EPI_TAIL && vec_ok) {
+                    // the output through TMA stores (OOB rows / columns / pixels are clipped):
+                    // the chunk's CH/32 boxes, lane = box row, 16-byte chunk c of a row at
+                    // physical chunk c ^ (row & 7) (SWIZZLE_128B)
+                    static_assert(CH % 32 == 0, "TMA-store chunks are 32 columns wide");
+                    const int buf = p.epi == 2 ? (ec & 1) : 0;
+                    ++ec;
+                    float* eb = epi_smem + buf * (Cfg::EPI_BYTES / 4) + q * (2 * Cfg::EPI_BOX);
+                    if (lane == 0) {  // the stores that last used this buffer have read it
+                        if (p.epi == 2) tc::bulk_wait_read<1>();
+                        else tc::bulk_wait_read<0>();
+                    }
+                    __syncwarp();
 #pragma unroll
-                for (int g = 0; g < CH / 16; ++g) {
-                    const int n = n0 + c0 + g * 16;
-                    // the output through TMA stores (OOB rows / columns / pixels are clipped)
-                    if (w.mode != EPI_TAIL && vec_ok) {
-                        float* eb = epi_smem + (q * 2 + (ebuf & 1)) * Cfg::EPI_BOX;
-                        if (lane == 0) tc::bulk_wait_read<1>();  // the store that last used this box has read it
-                        __syncwarp();
+                    for (int g = 0; g < CH / 16; ++g) {
+                        float* brow = eb + (g >> 1) * Cfg::EPI_BOX + lane * 32;
 #pragma unroll
-                        for (int v = 0; v < 4; ++v)
-                            *reinterpret_cast<uint4*>(eb + lane * 16 + 4 * v) =
+                        for (int v = 0; v < 4; ++v) {
+                            const int c = (g & 1) * 4 + v;
+                            *reinterpret_cast<uint4*>(brow + ((c ^ (lane & 7)) << 2)) =
                                 make_uint4(r[g][4 * v], r[g][4 * v + 1], r[g][4 * v + 2], r[g][4 * v + 3]);
-                        tc::fence_async_smem();
-                        __syncwarp();
-                        if (lane == 0) {
-                            const uint32_t src = tc::smem_u32(eb);
+                        }
+                    }
+                    tc::fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+#pragma unroll
+                        for (int b = 0; b < CH / 32; ++b) {
+                            const uint32_t src = tc::smem_u32(eb + b * Cfg::EPI_BOX);
+                            const int n = n0 + c0 + b * 32;
                             if constexpr (CONV) {
                                 if (red) tc::tma_red_add_4d(&tmY, src, n, bx1, bx2, bx3);
                                 else tc::tma_store_4d(&tmY, src, n, bx1, bx2, bx3);
@@ -447,11 +466,14 @@ __global__ void __launch_bounds__(192, 1)
                                 if (red) tc::tma_red_add_3d(&tmY, src, n, bx1, bx2);
                                 else tc::tma_store_3d(&tmY, src, n, bx1, bx2);
                             }
-                            tc::bulk_commit();
                         }
-                        ++ebuf;
-                        continue;
+                        tc::bulk_commit();
                     }
+                    continue;
+                }
+#pragma unroll
+                for (int g = 0; g < CH / 16; ++g) {
+                    const int n = n0 + c0 + g * 16;
                     if (!live || n >= ncols) continue;
                     if ((vec_ok || w.mode == EPI_TAIL) && n + 16 <= ncols) {
                         float* dst = w.mode == EPI_TAIL ? crow + (long long)(n / 16) * (128 * 16) : crow + n;
@@ -534,13 +556,13 @@ static bool encode(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* 
     return r == CUDA_SUCCESS;
 }
 
-// fp32 tensor (the output Y), no swizzle: a box lands row-major in shared memory
+// fp32 tensor (the output Y): 32-float (128-byte) box rows, 128B-swizzled in shared memory
 static bool encode_f32(CUtensorMap* m, void* ptr, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
                        const cuuint32_t* box, const cuuint32_t* es) {
     EncodeTiledFn enc = encode_tiled();
     if (!enc) return false;
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, ptr, dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -551,18 +573,18 @@ static bool encode_f32(CUtensorMap* m, void* ptr, int rank, const cuuint64_t* di
 // (512 columns per SM) and by the shared-memory bound; never more than one group per CG SMs
 // times that.
 template <int BN, int BK, int STAGES, int TQ, int CG>
-static long long tc_resident_groups(int num_sms) {
+static long long tc_resident_groups(int num_sms, int epi) {
     using Cfg = TcCfg<BN, BK, STAGES, CG>;
-    static std::atomic<long long> cache[64];
+    static std::atomic<long long> cache[64][2];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-    long long v = cache[dev & 63].load(std::memory_order_relaxed);
+    long long v = cache[dev & 63][epi - 1].load(std::memory_order_relaxed);
     if (v > 0) return v;
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(CG);
     cfg.blockDim = dim3(Cfg::THREADS);
-    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.dynamicSmemBytes = Cfg::smem(epi);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
@@ -575,13 +597,13 @@ static long long tc_resident_groups(int num_sms) {
         cudaGetLastError();
         clusters = 0;
     }
-    int per_sm = (int)((228 * 1024) / (Cfg::SMEM + 1024));
+    int per_sm = (int)((228 * 1024) / (Cfg::smem(epi) + 1024));
     const int tmem_per_sm = (int)(512 / Cfg::TMEM_COLS);
     per_sm = per_sm < tmem_per_sm ? per_sm : tmem_per_sm;
     per_sm = per_sm < 1 ? 1 : per_sm;
     long long g = (long long)(num_sms / CG) * per_sm;
     if (clusters > 0 && clusters < g) g = clusters;
-    cache[dev & 63].store(g, std::memory_order_relaxed);
+    cache[dev & 63][epi - 1].store(g, std::memory_order_relaxed);
     return g;
 }
 
@@ -601,7 +623,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     auto kern = tc_gemm_bf16_kernel<BN, BK, STAGES, TQ, CG>;
     static std::atomic<unsigned long long> optin{0};
     {
-        cudaError_t e = smem_optin(optin, kern, (int)Cfg::SMEM);
+        cudaError_t e = smem_optin(optin, kern, 227 * 1024);
         if (e != cudaSuccess) return e;
     }
     const ShapeInfo& s = *c.sh;
@@ -642,7 +664,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
         p.m_tiles = (int)((s.M + Cfg::BM - 1) / Cfg::BM);
         p.batch = (int)s.batch;
     }
-    // Y (fp32) for the TMA-store epilogue: one box = one epilogue warp's 32 rows x 16 columns
+    // Y (fp32) for the TMA-store epilogue: one box = one epilogue warp's 32 rows x 32 columns
     CUtensorMap ty;
     std::memset(&ty, 0, sizeof(ty));
     if (s.N % 4 == 0) {
@@ -651,13 +673,13 @@ cudaError_t tc_launch(const LaunchCtx& c) {
             constexpr int TQW = TQ < 32 ? TQ : 32;
             cuuint64_t yd[4] = {(cuuint64_t)s.k, (cuuint64_t)s.q, (cuuint64_t)s.p, (cuuint64_t)s.n};
             cuuint64_t ys[3] = {(cuuint64_t)s.k * 4, (cuuint64_t)(s.q * s.k * 4), (cuuint64_t)(s.p * s.q * s.k * 4)};
-            cuuint32_t yb[4] = {16, (cuuint32_t)TQW, (cuuint32_t)(32 / TQW), 1};
+            cuuint32_t yb[4] = {32, (cuuint32_t)TQW, (cuuint32_t)(32 / TQW), 1};
             cuuint32_t ye[4] = {1, 1, 1, 1};
             ok = encode_f32(&ty, c.y, 4, yd, ys, yb, ye);
         } else {
             cuuint64_t yd[3] = {(cuuint64_t)s.N, (cuuint64_t)s.M, (cuuint64_t)s.batch};
             cuuint64_t ys[2] = {(cuuint64_t)s.N * 4, (cuuint64_t)(s.M * s.N * 4)};
-            cuuint32_t yb[3] = {16, 32, 1};
+            cuuint32_t yb[3] = {32, 32, 1};
             cuuint32_t ye[3] = {1, 1, 1};
             ok = encode_f32(&ty, c.y, 3, yd, ys, yb, ye);
         }
@@ -670,6 +692,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     p.units = (int)units;
     p.sched = c.sched;
     p.raster = c.raster;
+    p.epi = c.epi == 2 ? 2 : 1;
     p.total_iters = tiles * p.kblocks;
     if (c.split > 1) {
         cudaError_t e = zero_for_splitk((float*)c.y, s.y_elems, c.stream);
@@ -678,7 +701,9 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     // persistent grid: as many CTA groups as can be co-resident (the stream-K flag protocol
     // spins heads on their tails, so every group MUST be resident at once): the occupancy
     // calculator's active clusters (registers, shared memory, cluster shape) capped by TMEM
-    const long long groups_max = tc_resident_groups<BN, BK, STAGES, TQ, CG>(c.num_sms);
+    const int epi = c.epi == 2 ? 2 : 1;
+    if (Cfg::smem(epi) > 227 * 1024) return cudaErrorInvalidConfiguration;
+    const long long groups_max = tc_resident_groups<BN, BK, STAGES, TQ, CG>(c.num_sms, epi);
     if (groups_max < 1) return cudaErrorInvalidConfiguration;
     long long groups = groups_max;
     if (c.sched >= 1) {
@@ -704,7 +729,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     std::memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)(groups * CG));
     cfg.blockDim = dim3(Cfg::THREADS);
-    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.dynamicSmemBytes = Cfg::smem(p.epi);
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;

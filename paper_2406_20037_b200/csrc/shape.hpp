@@ -26,8 +26,8 @@ enum SketchId : int32_t {
 // [win][ctv], fp32); used by the static validity rule and by the launcher
 inline size_t dwconv_smem_bytes(int rs, int ctv, int win) { return (size_t)4 * ((size_t)rs + win) * ctv; }
 
-// tcgen05 sketches: shared memory of the epilogue TMA-store staging (4 warps x 2 boxes x 32 x 16 fp32)
-constexpr int kTcEpiBytes = 4 * 2 * 32 * 16 * 4;
+// tcgen05 sketches: shared memory of the epilogue TMA-store staging (4 warps x 2 boxes x 32 x 32 fp32)
+constexpr int kTcEpiBytes = 4 * 2 * 32 * 32 * 4;
 
 // depthwise register-window schedule (ALG 0): taps + two input row segments (one in
 // flight) + accumulators must fit the register budget (fp32 values per thread)

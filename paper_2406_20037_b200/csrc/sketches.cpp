@@ -26,11 +26,14 @@ static std::vector<SketchDesc> build_catalogue() {
     // shared memory), k-parity FFMA2 accumulators; VEC = cp.async width, SPLIT_K as above.
     // OCC (runtime): 0 = one CTA per work unit (tile x k slice); k > 0 = k persistent CTAs per
     // SM walking the units, the cp.async ring running on into the next unit's tiles.
-    const std::vector<const char*> pipe_names = {"BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K", "OCC"};
+    // RED (runtime): split-K partial sums by 0 = vector atomics into a zeroed Y, 1 = a cluster of
+    // the tile's SPLIT_K CTAs reducing through distributed shared memory (SPLIT_K 2..8, OCC 0).
+    const std::vector<const char*> pipe_names = {"BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K", "OCC",
+                                                 "RED"};
     const std::vector<std::vector<int32_t>> pipe_vals = {{16, 32, 64, 128}, {32, 64, 128}, {8, 16, 32},
                                                          {2, 4},            {1, 2, 4},     {1, 4},
                                                          {2, 3, 4, 6},      {1, 2, 3, 4, 6, 8, 12, 16, 24, 32},
-                                                         {0, 1, 2, 3, 4}};
+                                                         {0, 1, 2, 3, 4},   {0, 1}};
     c.push_back({SK_SIMT_PIPE_GEMM_F32, "simt_pipe_gemm_f32", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL),
                  TUNER_F32, pipe_names, pipe_vals});
     c.push_back({SK_SIMT_PIPE_CONV_F32, "simt_pipe_conv_f32", 1 << TUNER_OP_CONV2D, TUNER_F32, pipe_names,
@@ -43,17 +46,21 @@ static std::vector<SketchDesc> build_catalogue() {
     // 2 = whole waves tile by tile + the remainder tiles cut into k-chunks, one per group.
     // RASTER (runtime): the order tiles are handed to the persistent CTAs, 0 = M fastest
     // (concurrent CTAs share the B panel), 1 = N fastest (they share the A panel).
-    const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER"};
+    // EPI (runtime): epilogue TMA-store staging buffer sets per warp, 1 or 2 (double-buffered:
+    // the next 64-column chunk is staged while the previous chunk's stores read the other set).
+    const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER", "EPI"};
     const std::vector<std::vector<int32_t>> tc_vals = {{128, 256}, {64, 128, 256}, {64, 128}, {2, 3, 4, 6},
-                                                       {1, 2, 4},  {0, 1, 2},       {0, 1}};
+                                                       {1, 2, 4},  {0, 1, 2},       {0, 1},    {1, 2}};
     c.push_back({SK_TC_GEMM_BF16, "tc_gemm_bf16", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL), TUNER_BF16,
                  tc_names, tc_vals});
     // implicit-GEMM conv: the 128-row M tile is a (128/TILE_Q) x TILE_Q rectangle of output pixels
-    const std::vector<const char*> tcc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "TILE_Q", "SCHED", "RASTER"};
-    std::vector<std::vector<int32_t>> tcc_vals(tc_vals.begin(), tc_vals.end() - 2);
+    const std::vector<const char*> tcc_names = {"BM",     "BN",    "BK",     "STAGES", "SPLIT_K",
+                                                "TILE_Q", "SCHED", "RASTER", "EPI"};
+    std::vector<std::vector<int32_t>> tcc_vals(tc_vals.begin(), tc_vals.end() - 3);
     tcc_vals.push_back({8, 16, 32});
     tcc_vals.push_back({0, 1, 2});
     tcc_vals.push_back({0, 1});
+    tcc_vals.push_back({1, 2});
     c.push_back({SK_TC_IGEMM_CONV_BF16, "tc_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tcc_names,
                  tcc_vals});
     // the SIMT implicit-GEMM sketch on bf16 inputs (widened to fp32 at staging, fp32
@@ -163,7 +170,8 @@ static bool simt_valid(const ShapeInfo& sh, const int32_t* v) {
 
 static bool pipe_valid(const ShapeInfo& sh, const int32_t* v) {
     const int bm = v[0], bn = v[1], bk = v[2], tt = v[3], kw = v[4], vec = v[5], stages = v[6], split = v[7],
-              occ = v[8];
+              occ = v[8], red = v[9];
+    if (red == 1 && (split < 2 || split > 8 || occ != 0)) return false;  // a portable cluster of the k slices
     const bool conv = sh.op == TUNER_OP_CONV2D;
     if (tt > bm || tt > bn) return false;
     const int gt = (bm / tt) * (bn / tt), threads = gt * kw;
@@ -221,8 +229,9 @@ static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
     }
     if (bn > 256 || (bm != 128 && bm != 256)) return false;
     const int cg = bm / 128;  // CTAs per tile: each stages 128 rows of A and bn/cg rows of B
+    const int epi = sh.op == TUNER_OP_CONV2D ? v[8] : v[7];
     const int64_t smem = (int64_t)stages * (128 + bn / cg) * bk * 2 + 1024 /*align*/ + 256 /*barriers*/ +
-                         kTcEpiBytes /*epilogue staging*/;
+                         (int64_t)epi * kTcEpiBytes /*epilogue staging*/;
     if (smem > 227 * 1024) return false;
     if (split > ktiles) return false;
     if ((int64_t)split * sh.batch > 65535) return false;

@@ -9,7 +9,7 @@ import torch
 
 from oracle import contractions as oc
 from oracle import numerics as on
-from paper_2406_20037_b200 import Tuner, global_launch_count, sketch_space, sketches
+from paper_2406_20037_b200 import Tuner, global_launch_count, knob_names, sketch_space, sketches
 from synth import tensors
 
 pytestmark = pytest.mark.gpu
@@ -371,3 +371,45 @@ def test_nccl_exchange_path_world1():
         t.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("sk,case", [(7, (1, 75, 53, 200)), (7, (3, 33, 40, 130)), (8, CONV_CASES[1]), (8, CONV_CASES[4]),
+                                     (8, (1, 14, 14, 64, 64, 3, 3, (1, 1), (1, 1), (1, 1)))])
+def test_pipe_cluster_splitk_vs_oracle(sk, case):
+    """RED = 1: the SPLIT_K CTAs of a tile form a thread-block cluster and reduce their partial
+    tiles through distributed shared memory (no zeroing kernel, no atomics): every such valid
+    schedule (sampled) equals the oracle, and on integer inputs bit for bit, also from a
+    replayed CUDA graph."""
+    space = sketch_space(sk)
+    ired = knob_names(sk).index("RED")
+    if sk == 7:
+        b, m, n, k = case
+        x, w = tensors([(b, m, k), (b, n, k)], sum(case), "int")
+        yo, _ = oc.bmm(x, w)
+        op, shape = ("dense" if b == 1 else "batch_matmul"), {"b": b, "m": m, "n": n, "k": k}
+    else:
+        nn, h, wd_, c, kk, r, s, st, pd, dl = case
+        x, w = tensors([(nn, h, wd_, c), (kk, r, s, c)], sum(case[:7]), "int")
+        yo, _ = oc.conv2d(x, w, st, pd, dl)
+        op, shape = "conv2d", {"N": nn, "H": h, "W": wd_, "C": c, "K": kk, "R": r, "S": s, "stride": st, "pad": pd,
+                               "dil": dl}
+    xd, wdd = to_dev(x, w)
+    y = torch.empty(yo.shape, device=dev())
+    t = Tuner(op, shape, spaces=[(sk, space)], x=xd, w=wdd, y=y)
+    pts = [p for p in all_points(sk) if p[1][ired] == 1 and t.valid(p)]
+    assert len(pts) > 20
+    for p, yv in run_points(t, random.Random(8).sample(pts, min(250, len(pts))), xd, wdd, y):
+        np.testing.assert_array_equal(yv.reshape(yo.shape), yo.astype(np.float32), err_msg=str(t.values(p)))
+    p = pts[0]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(3):
+                t.run(p, xd, wdd, y, stream=s)
+    y.fill_(float("nan"))
+    g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy().reshape(yo.shape), yo.astype(np.float32))
+    res = t.measure(pts[:16])
+    assert all(r.status == "ok" for r in res), [(t.values(r.point), r.status) for r in res if r.status != "ok"]
