@@ -141,6 +141,7 @@ static tuner_status wait_progress(const std::vector<cudaEvent_t>& evs, double st
 // launcher + runtime knobs of a point
 struct RuntimeKnobs {
     int split = 1, vec = 1, stages = 1, sched = 0, raster = 0, occ = 0, red = 0, epi = 1;
+    int cluster = 1;  // thread-block cluster size of the launch (a timing-graph cache key)
     int dims[3] = {1, 1, 1};
 };
 static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
@@ -163,18 +164,21 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
             rk.split = v[7];
             rk.occ = v[8];
             rk.red = v[9];
+            rk.cluster = v[9] == 1 ? v[7] : 1;
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[4] | (v[5] << 4)));
         case SK_TC_GEMM_BF16:  // BM, BN, BK, STAGES, SPLIT_K, SCHED, RASTER, EPI
             rk.split = v[4];
             rk.sched = v[5];
             rk.raster = v[6];
             rk.epi = v[7];
+            rk.cluster = v[0] / 128;
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], 0));
         case SK_TC_IGEMM_CONV_BF16:  // BM, BN, BK, STAGES, SPLIT_K, TILE_Q, SCHED, RASTER, EPI
             rk.split = v[4];
             rk.sched = v[6];
             rk.raster = v[7];
             rk.epi = v[8];
+            rk.cluster = v[0] / 128;
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[5]));
         case SK_SIMT_DIRECT_CONV_F32:  // KT, TP (compiled) | PX, BKC, EPI
         case SK_SIMT_DIRECT_CONV_BF16:
@@ -237,14 +241,18 @@ struct GpuMeasurer : Measurer {
     // cudaGraphExecUpdate (kernel function, grid and arguments may change), which is
     // far cheaper on the host than cudaGraphInstantiate.  Launches already enqueued
     // keep the parameters they were launched with.
-    std::vector<std::pair<size_t, cudaGraphExec_t>> exec_cache;
+    // Cache key: (node count, sketch, cluster size).  cudaGraphExecUpdate does not carry a kernel
+    // node's launch attributes over (a cluster dimension in particular), so an executable is
+    // only ever updated with a graph of the same sketch and cluster shape.
+    std::vector<std::pair<uint64_t, cudaGraphExec_t>> exec_cache;
 
-    cudaError_t exec_for(cudaGraph_t g, cudaGraphExec_t& out) {
+    cudaError_t exec_for(cudaGraph_t g, uint64_t family, cudaGraphExec_t& out) {
         size_t nn = 0;
         cudaError_t e = cudaGraphGetNodes(g, nullptr, &nn);
         if (e != cudaSuccess) return e;
+        const uint64_t key = ((uint64_t)nn << 32) | family;
         for (auto& ce : exec_cache) {
-            if (ce.first != nn) continue;
+            if (ce.first != key) continue;
             cudaGraphExecUpdateResultInfo info;
             if (cudaGraphExecUpdate(ce.second, g, &info) == cudaSuccess) {
                 out = ce.second;
@@ -254,7 +262,7 @@ struct GpuMeasurer : Measurer {
         }
         e = cudaGraphInstantiate(&out, g, 0);
         if (e != cudaSuccess) return e;
-        if (exec_cache.size() < kExecCache) exec_cache.emplace_back(nn, out);
+        if (exec_cache.size() < kExecCache) exec_cache.emplace_back(key, out);
         else transient.push_back(out);  // destroyed after this phase's synchronisation
         return cudaSuccess;
     }
@@ -312,6 +320,7 @@ struct GpuMeasurer : Measurer {
         size_t n = 0;
         std::vector<LaunchFn> fn;
         std::vector<RuntimeKnobs> rk;
+        std::vector<int32_t> pos;  // position of each candidate's sketch in the tuner's space list
         std::vector<char> launched, cut, precise;
         std::vector<double> tver;
         std::vector<int> reps, warm, number, nlong;
@@ -352,7 +361,11 @@ struct GpuMeasurer : Measurer {
         set_capturing(false);
         if (e != cudaSuccess) return cuda_fail(e, "graph capture");
         if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamEndCapture");
-        e = exec_for(g, b.execs[j]);
+        // family: sketch, cluster size, and whether a split-K zeroing node precedes each launch
+        // (programmatic edges) -- launch attributes a cached executable cannot take over
+        const uint64_t fam = ((uint64_t)(t->spaces[b.pos[j]].sketch & 0xFFFF) << 16) |
+                             ((uint64_t)(b.rk[j].split > 1) << 15) | (uint64_t)(b.rk[j].cluster & 0x7FFF);
+        e = exec_for(g, fam, b.execs[j]);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
         CU(cudaEventRecord(ev[base], st));
@@ -388,6 +401,7 @@ struct GpuMeasurer : Measurer {
         bool need_sk = false;
         for (size_t j = 0; j < n; ++j) {
             b.fn[j] = resolve(t, pts[j], b.rk[j]);
+            b.pos[j] = pts[j].pos;
             need_sk |= b.rk[j].sched >= 1;
         }
         if (need_sk && (s = ensure_streamk(t, st)) != TUNER_OK) return s;
@@ -575,6 +589,7 @@ struct GpuMeasurer : Measurer {
         if (n == 0 && !coll) return TUNER_OK;
         b.fn.assign(n, nullptr);
         b.rk.assign(n, RuntimeKnobs{});
+        b.pos.assign(n, 0);
         b.launched.assign(n, 0);
         b.cut.assign(n, 0);
         b.precise.assign(n, 0);

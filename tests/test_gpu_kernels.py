@@ -413,3 +413,30 @@ def test_pipe_cluster_splitk_vs_oracle(sk, case):
     np.testing.assert_array_equal(y.cpu().numpy().reshape(yo.shape), yo.astype(np.float32))
     res = t.measure(pts[:16])
     assert all(r.status == "ok" for r in res), [(t.values(r.point), r.status) for r in res if r.status != "ok"]
+
+
+def test_batched_costs_mixed_launch_shapes():
+    """The timing-graph executable cache (cudaGraphExecUpdate) never carries one candidate's
+    launch shape over to another: a batch interleaving split-K schedules reduced by atomics
+    (zeroing node + programmatic edge), by a thread-block cluster (RED = 1, cluster dims), and
+    plain launches of the same sketch gives every candidate its one-at-a-time cost."""
+    n, h, wd_, c, k = 1, 28, 28, 128, 128
+    x, w = tensors([(n, h, wd_, c), (k, 3, 3, c)], 41)
+    xd, wdd = to_dev(x, w)
+    y = torch.empty(n, h, wd_, k, device=dev())
+    shape = {"N": n, "H": h, "W": wd_, "C": c, "K": k, "R": 3, "S": 3, "stride": (1, 1), "pad": (1, 1)}
+    sp = sketch_space(8)
+    pick = lambda vals: (8, tuple(sp[d].index(v) for d, v in enumerate(vals)))  # noqa: E731
+    pts = [pick([32, 64, 32, 4, 1, 4, 2, 6, 0, 1]), pick([16, 64, 32, 4, 1, 4, 2, 1, 0, 0]),
+           pick([32, 64, 32, 4, 1, 4, 2, 6, 0, 0]), pick([64, 64, 16, 4, 1, 4, 2, 4, 0, 1]),
+           pick([16, 128, 32, 4, 2, 4, 3, 1, 0, 0]), pick([64, 64, 16, 4, 1, 4, 2, 4, 0, 0])]
+    single = {}
+    for p in pts:
+        t1 = Tuner("conv2d", shape, spaces=[(8, sp)], x=xd, w=wdd, y=y, seed=1)
+        assert t1.valid(p), t1.values(p)
+        single[p] = t1.measure([p])[0].cost_ns
+        t1.close()
+    t = Tuner("conv2d", shape, spaces=[(8, sp)], x=xd, w=wdd, y=y, seed=2)
+    for p, r in zip(pts, t.measure(pts)):
+        assert r.status == "ok"
+        assert 0.7 < r.cost_ns / single[p] < 1.4, (t.values(p), r.cost_ns, single[p])

@@ -76,7 +76,9 @@ def run(args):
 def parse(args):
     import bench
     recs, dtype = bench_layers(args.bench)
-    rows = list(csv.reader(open(args.csv)))
+    lines = open(args.csv).read().splitlines()
+    start = next(i for i, ln in enumerate(lines) if ln.startswith('"ID"'))  # skip ncu's log lines
+    rows = list(csv.reader(lines[start:]))
     hdr = rows[0]
     ix = {h: i for i, h in enumerate(hdr)}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}

@@ -11,7 +11,7 @@ prof() {  # name layer sketch values dtype kernel-regex
   ncu -i gpurun_out/prof_$1.ncu-rep --page details --csv > gpurun_out/prof_$1.details.csv 2>/dev/null
   rm -f gpurun_out/prof_$1.ncu-rep
 }
-prof r2_tc_ffn1 bert.ffn1 2 ${FFN1:-256,256,64,6,1,0,1} bf16 tc_gemm
-prof r2_pipe_r18l1 r18.l1.3x3 8 ${R18L1:-64,64,32,4,1,4,3,6,0} f32 simt_pipe
+prof r2_tc_ffn1 bert.ffn1 2 ${FFN1:-256,256,64,6,1,0,1,1} bf16 tc_gemm
+prof r2_pipe_r18l1 r18.l1.3x3 8 ${R18L1:-64,64,32,4,1,4,3,6,0,0} f32 simt_pipe
 DB200_TC_TRACE=1 python tools/time_schedule.py --layer bert.ffn1 --dtype bf16 --sketch 2 \
-  --values ${FFN1:-256,256,64,6,1,0,1} --iters 1 > gpurun_out/r2_tc_trace_ffn1.txt 2>&1
+  --values ${FFN1:-256,256,64,6,1,0,1,1} --iters 1 > gpurun_out/r2_tc_trace_ffn1.txt 2>&1
