@@ -116,6 +116,8 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
     const int kz = blockIdx.z % p.split;
     const int kt_begin = kz * p.kt_per_split;
     const int kt_end = min(p.ktiles, kt_begin + p.kt_per_split);
+    // programmatic dependent launch: the next kernel in the stream may start its own prologue now
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (kt_begin >= kt_end) return;
 
     const TIn* __restrict__ A = (const TIn*)p.A + (CONV ? 0 : bz * p.sA);
@@ -310,6 +312,10 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
         }
     };
 
+    // launched with programmatic stream serialization: the prologue above overlaps the preceding
+    // kernel's tail; X and W are read only after it completed (behind this schedule's own split-K
+    // zeroing kernel, itself fully serialised, the wait is deferred to the first atomic)
+    if (p.split == 1) griddep_wait();
     if (p.stages >= 2) {  // STAGES = 2: register prefetch of the next tile overlaps the FMAs
         gload(kt_begin);
         sstore(0);
@@ -400,12 +406,10 @@ cudaError_t simt_launch(const LaunchCtx& c) {
     cfg.blockDim = dim3(Cfg::NT);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
-    if (c.split > 1) {  // launch early; the kernel waits for the zeroing before its atomics
-        pdl_attr(attr[0]);
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-    }
+    cudaLaunchAttribute attr[1];  // always a programmatic dependent launch (see the kernel)
+    pdl_attr(attr[0]);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
     count_launches(1);
     if (e != cudaSuccess) return e;

@@ -104,6 +104,8 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
     const int tx = gt % TX, ty = gt / TX;
     constexpr int CPR = BK / VW;  // cp.async chunks per tile row
     const int u0 = blockIdx.x, ustep = gridDim.x;
+    // programmatic dependent launch: the next kernel in the stream may start its own prologue now
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (u0 >= p.units) return;
 
     // unit -> (k slice, m tile, n tile, batch), k slice fastest
@@ -400,6 +402,11 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
             }
         }
     };
+    // Launched with programmatic stream serialization: the prologue above (k table, slot setup)
+    // overlaps the preceding kernel's tail.  X and W are read only after that kernel completed --
+    // except behind this schedule's own split-K zeroing kernel (launched fully serialised, so
+    // every earlier kernel is complete), where the wait is deferred to the first atomic.
+    if (!atomic) griddep_wait();
     for (int s = 0; s < stages - 1; ++s) {
         produce(s);
         cp_commit();
@@ -478,18 +485,18 @@ cudaError_t pipe_launch(const LaunchCtx& c) {
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
+    // always a programmatic dependent launch (after the zeroing kernel, the kernel waits before
+    // its first atomic; otherwise before its first load)
+    cudaLaunchAttribute attr[2];
+    pdl_attr(attr[0]);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     if (p.cred) {
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = (unsigned)c.split;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-    } else if (c.split > 1) {  // launch early; the kernel waits for the zeroing before its atomics
-        pdl_attr(attr[0]);
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = (unsigned)c.split;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = 1;
+        cfg.numAttrs = 2;
     }
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
     count_launches(1);

@@ -55,12 +55,13 @@ struct TcCfg {
     // 32-row x 32-column fp32 boxes whose 128-byte rows are stored 128B-swizzled (bank-conflict
     // free st.shared.v4, and the layout the tensor map's SWIZZLE_128B expects), written with ONE
     // proxy fence and two TMA stores per chunk; 1024-byte aligned, right after the stages
-    // (EPI knob: 1 or 2 such buffer sets; with 2 a warp writes chunk c while chunk c-1's stores
-    // still read the other set)
+    // (EPI knob: 1 = the boxes go out as TMA stores; 2 = the warp reads its boxes back row-major
+    // and writes them with coalesced 128-byte st.global / red.global segments -- no async proxy,
+    // no TMA queue shared with the operand loads)
     static constexpr int EPI_BOX = 32 * 32;
     static constexpr int EPI_BYTES = 4 * 2 * EPI_BOX * 4;
     static_assert(EPI_BYTES == kTcEpiBytes, "epilogue staging size");
-    static constexpr size_t smem(int epi) { return 1024 + (size_t)STAGES * STAGE_BYTES + (size_t)epi * EPI_BYTES + 256; }
+    static constexpr size_t smem(int) { return 1024 + (size_t)STAGES * STAGE_BYTES + (size_t)EPI_BYTES + 256; }
     static constexpr int THREADS = 192;
 };
 
@@ -72,7 +73,7 @@ struct TcParams {
     int units;                    // SCHED 0: batch * mp_tiles * n_tiles * split
     int sched;                    // 0 = tiles (+ split-K), 1 = stream-K, 2 = full waves by tile + k-chunked rest
     int raster;                   // tile order: 0 = M fastest, 1 = N fastest
-    int epi;                      // EPI knob: epilogue staging buffer sets per warp (1 or 2)
+    int epi;                      // EPI knob: 1 = TMA-store epilogue, 2 = coalesced st.global epilogue
     int dp_tiles;                 // SCHED 2: tiles handled whole (a multiple of the group count)
     int rem_tiles, rem_chunks;    // SCHED 2: remainder tiles and k-chunks per remainder tile
     long long total_iters;        // SCHED 1/2: streamed k-block iterations (tiles - dp_tiles) * kblocks
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(192, 1)
     constexpr int TP = CONV ? BM / TQ : 1;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(base + STAGES * Cfg::STAGE_BYTES + p.epi * Cfg::EPI_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES);
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
     uint64_t* acc_full = bars + 2 * STAGES;       // [2] MMA -> epilogue
@@ -339,7 +340,6 @@ __global__ void __launch_bounds__(192, 1)
         const int q = warp & 3;
         const int trow = q * 32 + lane;  // row of the 128-row sub-tile held by this thread
         const bool vec_ok = (p.N % 4) == 0;  // TMA needs 16-byte global strides
-        int ec = 0;                          // TMA-stored chunks so far (staging buffer = ec % EPI)
         int j = 0;
         SegIter si(p, group, ngroups);
         Seg w;
@@ -430,45 +430,70 @@ __global__ void __launch_bounds__(192, 1)
                     }
                 }
                 if (w.mode != EPI_TAIL && vec_ok) {
-                    // the output through TMA stores (OOB rows / columns / pixels are clipped):
-                    // the chunk's CH/32 boxes, lane = box row, 16-byte chunk c of a row at
-                    // physical chunk c ^ (row & 7) (SWIZZLE_128B)
-                    static_assert(CH % 32 == 0, "TMA-store chunks are 32 columns wide");
-                    const int buf = p.epi == 2 ? (ec & 1) : 0;
-                    ++ec;
-                    float* eb = epi_smem + buf * (Cfg::EPI_BYTES / 4) + q * (2 * Cfg::EPI_BOX);
-                    if (lane == 0) {  // the stores that last used this buffer have read it
-                        if (p.epi == 2) tc::bulk_wait_read<1>();
-                        else tc::bulk_wait_read<0>();
+                    // staged through shared memory: the chunk's CH/32 boxes of 32 rows x 32
+                    // columns, lane = box row, 16-byte chunk c of a row at physical chunk
+                    // c ^ (row & 7) (SWIZZLE_128B: conflict-free st.shared.v4 / ld.shared.v4)
+                    static_assert(CH % 32 == 0, "staged chunks are 32 columns wide");
+                    const uint32_t eb = tc::smem_u32(epi_smem + q * (2 * Cfg::EPI_BOX));
+                    if (p.epi == 1) {
+                        if (lane == 0) tc::bulk_wait_read<0>();  // the previous chunk's stores have read it
+                        __syncwarp();
                     }
-                    __syncwarp();
 #pragma unroll
                     for (int g = 0; g < CH / 16; ++g) {
-                        float* brow = eb + (g >> 1) * Cfg::EPI_BOX + lane * 32;
+                        const uint32_t brow = eb + (uint32_t)((g >> 1) * Cfg::EPI_BOX * 4 + lane * 128);
 #pragma unroll
                         for (int v = 0; v < 4; ++v) {
                             const int c = (g & 1) * 4 + v;
-                            *reinterpret_cast<uint4*>(brow + ((c ^ (lane & 7)) << 2)) =
-                                make_uint4(r[g][4 * v], r[g][4 * v + 1], r[g][4 * v + 2], r[g][4 * v + 3]);
+                            tc::st_shared_v4(brow + (uint32_t)((c ^ (lane & 7)) << 4), r[g][4 * v], r[g][4 * v + 1],
+                                             r[g][4 * v + 2], r[g][4 * v + 3]);
                         }
                     }
-                    tc::fence_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
+                    if (p.epi == 1) {  // TMA stores (OOB rows / columns / pixels are clipped by the map)
+                        tc::fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
 #pragma unroll
-                        for (int b = 0; b < CH / 32; ++b) {
-                            const uint32_t src = tc::smem_u32(eb + b * Cfg::EPI_BOX);
-                            const int n = n0 + c0 + b * 32;
-                            if constexpr (CONV) {
-                                if (red) tc::tma_red_add_4d(&tmY, src, n, bx1, bx2, bx3);
-                                else tc::tma_store_4d(&tmY, src, n, bx1, bx2, bx3);
-                            } else {
-                                if (red) tc::tma_red_add_3d(&tmY, src, n, bx1, bx2);
-                                else tc::tma_store_3d(&tmY, src, n, bx1, bx2);
+                            for (int b = 0; b < CH / 32; ++b) {
+                                const uint32_t src = eb + (uint32_t)(b * Cfg::EPI_BOX * 4);
+                                const int n = n0 + c0 + b * 32;
+                                if constexpr (CONV) {
+                                    if (red) tc::tma_red_add_4d(&tmY, src, n, bx1, bx2, bx3);
+                                    else tc::tma_store_4d(&tmY, src, n, bx1, bx2, bx3);
+                                } else {
+                                    if (red) tc::tma_red_add_3d(&tmY, src, n, bx1, bx2);
+                                    else tc::tma_store_3d(&tmY, src, n, bx1, bx2);
+                                }
                             }
+                            tc::bulk_commit();
                         }
-                        tc::bulk_commit();
+                        continue;
                     }
+                    // EPI 2: read the boxes back row-major, 8 lanes per 128-byte row segment, 4 rows
+                    // per instruction, and write coalesced segments (rows / columns past the edge
+                    // skipped; a row's global base comes from the lane that owns the row)
+                    __syncwarp();
+                    const int sub = lane >> 3, c = lane & 7;
+#pragma unroll
+                    for (int b = 0; b < CH / 32; ++b) {
+                        const int n = n0 + c0 + b * 32 + 4 * c;
+#pragma unroll 4
+                        for (int it = 0; it < 8; ++it) {
+                            const int rr = it * 4 + sub;
+                            const float* rbase = reinterpret_cast<const float*>(
+                                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(crow), rr));
+                            const bool rok = __shfl_sync(0xffffffffu, live ? 1 : 0, rr) != 0;
+                            uint32_t v0, v1, v2, v3;
+                            tc::ld_shared_v4(eb + (uint32_t)(b * Cfg::EPI_BOX * 4 + rr * 128 + ((c ^ (rr & 7)) << 4)),
+                                             v0, v1, v2, v3);
+                            if (!rok || n >= ncols) continue;
+                            float* dst = const_cast<float*>(rbase) + n;
+                            if (red) tc::red_add_v4(dst, __uint_as_float(v0), __uint_as_float(v1), __uint_as_float(v2),
+                                                    __uint_as_float(v3));
+                            else *reinterpret_cast<uint4*>(dst) = make_uint4(v0, v1, v2, v3);
+                        }
+                    }
+                    __syncwarp();  // every lane has read the boxes before the next chunk restages them
                     continue;
                 }
 #pragma unroll
