@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--explore", default="evolve", choices=["evolve", "random"],
                     help="exploration phase of DPAnsor: Ansor-style evolution (default) or uniform sampling")
     ap.add_argument("--droplet-budget", type=int, default=100)
+    ap.add_argument("--droplet-sketch-factor", type=float, default=1.5,
+                    help="Droplet also starts from the best point of every other sketch within this factor "
+                         "of the overall best (R-D17); 1.0 = the paper's single start")
     ap.add_argument("--baseline", type=int, default=10000)
     ap.add_argument("--early-cut", type=float, default=4.0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -325,13 +328,22 @@ def main():
             rec.update(skipped="no statically valid schedule", candidates=0, launches=0, collectives=0)
             return rec
         b = tu.best()
-        rep = tu.droplet(b.point, args.droplet_budget)
+        # Droplet moves inside one sketch's space: it starts from the best point of
+        # every sketch whose best is within DROPLET_SKETCH_FACTOR of the overall best (R-D17)
+        starts = []
+        for sid, _ in tu.spaces:
+            sb = tu.best_of_sketch(sid)
+            if sb is not None and sb.cost_ns <= args.droplet_sketch_factor * b.cost_ns:
+                starts.append(sb)
+        reps = [tu.droplet(sb.point, args.droplet_budget) for sb in sorted(starts, key=lambda x: x.cost_ns)]
+        rep = min(reps, key=lambda r: r["best_cost"])
         t1 = time.perf_counter()
         st = tu.stats()
         rec.update(dp_best_ns=rep["best_cost"], dp_point=rep["best"], sketch=rep["best"][0],
-                   dp_best=tu.values(rep["best"]),
-                   sample_best_ns=b.cost_ns, droplet_trials=rep["trials_used"], droplet_rounds=rep["rounds"],
-                   converged=rep["converged"], dp_wall_s=t1 - t0, dp_candidates=st["candidates"],
+                   dp_best=tu.values(rep["best"]), droplet_starts=len(reps),
+                   sample_best_ns=b.cost_ns, droplet_trials=sum(r["trials_used"] for r in reps),
+                   droplet_rounds=sum(r["rounds"] for r in reps),
+                   converged=all(r["converged"] for r in reps), dp_wall_s=t1 - t0, dp_candidates=st["candidates"],
                    launches=st["kernel_launches"], collectives=st["collectives"],
                    wrong=sum(s.status != "ok" for s in tu.history()))
         cut, precise = st["early_cut"], st["precise"]

@@ -278,6 +278,12 @@ tuner_status tuner_timings(const tuner_t* t, const tuner_point* pt, float* out, 
 /* Best-of-N: first argmin of cost over history (R-B1).  ESTATE if empty. */
 tuner_status tuner_best(const tuner_t* t, tuner_result* out);
 
+/* The same restricted to one sketch's points: the start of a per-sketch Droplet Search
+ * (R-D17: Droplet moves inside one sketch's space, so DPAnsor over several sketches
+ * hands each sketch's best configuration to its own Droplet run).  ERANGE if the sketch is not
+ * in this tuner's spaces; ESTATE if none of its points has a finite cost. */
+tuner_status tuner_best_of_sketch(const tuner_t* t, int32_t sketch, tuner_result* out);
+
 /* All measured samples in measurement order. */
 tuner_status tuner_history(const tuner_t* t, tuner_result* out, int64_t cap, int64_t* n_out);
 

@@ -268,6 +268,15 @@ class OracleTuner:
                 bp, bc = p, c
         return bp, bc
 
+    def best_of_sketch(self, s: int) -> Optional[Tuple[Point, float]]:
+        """First argmin over the history points of sketch s with a finite cost (R-B1 restricted to
+        one sketch: the start of that sketch's Droplet run, R-D17); None if there is none."""
+        found = None
+        for p, c in self.history:
+            if p[0] == s and math.isfinite(c) and (found is None or c < found[1]):
+                found = (p, c)
+        return found
+
     # ------------------------------------------------------------------ Droplet Search
     def droplet(self, start: Point, budget: int = 100, policy: str = "plain", alpha: float = 0.0) -> dict:
         """Droplet Search, PAPER.md P:297-304:

@@ -93,6 +93,7 @@ SIGNATURES = {
     "tuner_droplet": (C.c_int, [C.c_void_p, C.POINTER(Point), C.c_int32, C.POINTER(Point), C.c_int32,
                                 C.POINTER(DropletReport)]),
     "tuner_best": (C.c_int, [C.c_void_p, C.POINTER(Result)]),
+    "tuner_best_of_sketch": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Result)]),
     "tuner_timings": (C.c_int, [C.c_void_p, C.POINTER(Point), C.POINTER(C.c_float), C.c_int32, C.POINTER(C.c_int32)]),
     "tuner_history": (C.c_int, [C.c_void_p, C.POINTER(Result), C.c_int64, C.POINTER(C.c_int64)]),
     "kernel_run": (C.c_int, [C.c_void_p, C.POINTER(Point), C.POINTER(Buffers), C.c_void_p]),

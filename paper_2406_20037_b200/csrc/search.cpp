@@ -982,6 +982,24 @@ extern "C" tuner_status tuner_best(const tuner_t* tc, tuner_result* out) {
     return TUNER_OK;
 }
 
+extern "C" tuner_status tuner_best_of_sketch(const tuner_t* tc, int32_t sketch, tuner_result* out) {
+    Tuner* t = const_cast<tuner_t*>(tc);
+    CHECK_HANDLE(t);
+    if (!out) return fail(TUNER_EINVAL, "NULL out");
+    bool known = false;
+    for (const auto& sp : t->spaces) known |= sp.sketch == sketch;
+    if (!known) return fail(TUNER_ERANGE, "sketch not in this tuner's spaces");
+    size_t bi = t->history.size();
+    for (size_t i = 0; i < t->history.size(); ++i) {
+        const tuner_result& h = t->history[i];
+        if (h.pt.sketch != sketch || !std::isfinite(h.cost_ns)) continue;
+        if (bi == t->history.size() || h.cost_ns < t->history[bi].cost_ns) bi = i;  // first argmin (R-B1)
+    }
+    if (bi == t->history.size()) return fail(TUNER_ESTATE, "no finite measurement of this sketch");
+    *out = t->history[bi];
+    return TUNER_OK;
+}
+
 extern "C" tuner_status tuner_history(const tuner_t* tc, tuner_result* out, int64_t cap, int64_t* n_out) {
     Tuner* t = const_cast<tuner_t*>(tc);
     if (!t) return fail(TUNER_EINVAL, "NULL tuner handle");

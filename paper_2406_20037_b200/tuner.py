@@ -284,6 +284,16 @@ class Tuner:
         L.check(L.lib().tuner_best(self._h, C.byref(r)))
         return _sample(r)
 
+    def best_of_sketch(self, sketch: int) -> Optional[Sample]:
+        """First argmin among one sketch's measured points (tuner_best_of_sketch); None if it has
+        no finite measurement."""
+        r = L.Result()
+        st = L.lib().tuner_best_of_sketch(self._h, sketch, C.byref(r))
+        if st == L.ESTATE:
+            return None
+        L.check(st)
+        return _sample(r)
+
     def history(self) -> List[Sample]:
         n = C.c_int64()
         L.check(L.lib().tuner_history(self._h, None, 0, C.byref(n)))

@@ -153,3 +153,31 @@ def test_sampler_hand_trace_product():
     t = Tuner("dense", {"m": 1, "n": 1, "k": 1}, spaces=[(0, [[10, 20]]), (1, [[1, 2, 3]])],
               cost_table=[1.0, 2.0, 3.0, math.inf, 5.0], seed=0)
     assert [s.point for s in t.sample(2)] == [(0, (1,)), (0, (0,))]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_per_sketch_droplet_bit_exact(seed):
+    # R-D17: after exploration, Droplet from each sketch's best point (tuner_best_of_sketch): the
+    # starts, trajectories and final best match the oracle bit for bit in cost-table mode
+    rng = random.Random(seed + 40)
+    sk = [[list(range(rng.randint(2, 5))) for _ in range(rng.randint(2, 4))] for _ in range(3)]
+    table = landscape([[len(v) for v in s] for s in sk], "rugged", seed, 0.1)
+    sp = Space(sk)
+    c, v = table_cost(sp, table)
+    o = OracleTuner(sp, c, v, seed)
+    o.sample(20)
+    t = Tuner("dense", {"m": 1, "n": 1, "k": 1}, spaces=[(i, s) for i, s in enumerate(sk)], cost_table=table,
+              seed=seed)
+    t.sample(20)
+    for s_ in range(3):
+        ob = o.best_of_sketch(s_)
+        tb = t.best_of_sketch(s_)
+        assert (ob is None) == (tb is None)
+        if ob is None:
+            continue
+        assert (ob[0][0], ob[0][1], ob[1]) == (tb.point[0], tb.point[1], tb.cost_ns)
+        orep = o.droplet(ob[0], 40, "grow")
+        trep = t.droplet(tb.point, 40)
+        assert [p[1] for p in orep["traj"]] == [p[1] for p in trep["traj"]]
+        assert (orep["trials_used"], orep["rounds"]) == (trep["trials_used"], trep["rounds"])
+    assert o.best()[1] == t.best().cost_ns

@@ -12,8 +12,7 @@ form -- never against the oracle's own code):
   very short time are removed from this worklist"; R-F3) -- hand-derived trial splits;
 * SURVEY §8(c)'s closed-form trial and round counts for sum (v_i - 3)^2 on {0..9}^4.
 
-Each docstring states the hand derivation.  tests/test_oracle_pins_r2.py::test_*_mutants
-re-runs the pins against deliberately broken oracle variants to show they bite.
+Each docstring states the hand derivation.  tests/test_pin_mutants.py re-runs the pins against deliberately broken oracle variants to show they bite.
 """
 import json
 import math
@@ -169,3 +168,17 @@ def test_grow_closed_form_counts():
     assert rep["rounds"] == 17 and rep["trials_used"] == 75 + 1 and rep["converged"]
     assert [p[1] for p in rep["traj"][:3]] == [(0, 0, 0, 0), (1, 0, 0, 0), (2, 0, 0, 0)]
     assert rep["best"] == (0, (3, 3, 3, 3))
+
+
+def test_best_of_sketch_by_hand():
+    """R-D17 start points: history (measurement order) = (1,(0,)) 5, (0,(1,)) 3, (1,(2,)) 2, (0,(0,)) 3,
+    (1,(1,)) 2, (0,(2,)) inf: sketch 0 -> (0,(1,)) (first of the tied 3s), sketch 1 -> (1,(2,)) (first of
+    the tied 2s), a sketch with no finite cost -> None."""
+    sp = Space([[[0, 1, 2]], [[0, 1, 2]], [[0]]])
+    cost = {(1, (0,)): 5.0, (0, (1,)): 3.0, (1, (2,)): 2.0, (0, (0,)): 3.0, (1, (1,)): 2.0, (0, (2,)): math.inf,
+            (2, (0,)): math.inf}
+    t = OracleTuner(sp, lambda p: cost[p], lambda p: True)
+    t.measure([(1, (0,)), (0, (1,)), (1, (2,)), (0, (0,)), (1, (1,)), (0, (2,)), (2, (0,))])
+    assert t.best_of_sketch(0) == ((0, (1,)), 3.0)
+    assert t.best_of_sketch(1) == ((1, (2,)), 2.0)
+    assert t.best_of_sketch(2) is None
