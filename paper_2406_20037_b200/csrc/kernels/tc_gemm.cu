@@ -43,14 +43,16 @@
 namespace db200 {
 
 
-template <int BN, int BK, int STAGES, int CG>
+// STAGES is a runtime knob (the ring depth only sizes shared memory and indexes the ring)
+template <int BN, int BK, int CG>
 struct TcCfg {
     static constexpr int BM = 128;  // rows of A per CTA
     static constexpr int BNC = BN / CG;  // rows of B per CTA
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BNC * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
+    // double-buffered accumulator, allocated as a power of two >= 32 columns (BN = 192 -> 512)
+    static constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
     // epilogue staging for TMA stores: per epilogue warp one 64-column TMEM chunk = two
     // 32-row x 32-column fp32 boxes whose 128-byte rows are stored 128B-swizzled (bank-conflict
     // free st.shared.v4, and the layout the tensor map's SWIZZLE_128B expects), written with ONE
@@ -61,7 +63,8 @@ struct TcCfg {
     static constexpr int EPI_BOX = 32 * 32;
     static constexpr int EPI_BYTES = 4 * 2 * EPI_BOX * 4;
     static_assert(EPI_BYTES == kTcEpiBytes, "epilogue staging size");
-    static constexpr size_t smem(int) { return 1024 + (size_t)STAGES * STAGE_BYTES + (size_t)EPI_BYTES + 256; }
+    static constexpr int MAX_STAGES = 8;
+    static constexpr size_t smem(int stages) { return 1024 + (size_t)stages * STAGE_BYTES + (size_t)EPI_BYTES + 256; }
     static constexpr int THREADS = 192;
 };
 
@@ -74,6 +77,7 @@ struct TcParams {
     int sched;                    // 0 = tiles (+ split-K), 1 = stream-K, 2 = full waves by tile + k-chunked rest
     int raster;                   // tile order: 0 = M fastest, 1 = N fastest
     int epi;                      // EPI knob: 1 = TMA-store epilogue, 2 = coalesced st.global epilogue
+    int stages;                   // STAGES knob: depth of the TMA -> MMA shared-memory ring
     int dp_tiles;                 // SCHED 2: tiles handled whole (a multiple of the group count)
     int rem_tiles, rem_chunks;    // SCHED 2: remainder tiles and k-chunks per remainder tile
     long long total_iters;        // SCHED 1/2: streamed k-block iterations (tiles - dp_tiles) * kblocks
@@ -166,16 +170,26 @@ struct SegIter {
             cur += s.nkb;
         }
         s.tile = t;
+        const int per = p.mp_tiles * p.n_tiles;
+        s.bz = t / per;
+        int r = t - s.bz * per;
         if (p.raster == 0) {  // m fastest: concurrent CTAs share the B (weight) panel in L2
-            s.mt = t % p.mp_tiles;
-            t /= p.mp_tiles;
-            s.nt = t % p.n_tiles;
-        } else {  // n fastest: concurrent CTAs share the A panel
-            s.nt = t % p.n_tiles;
-            t /= p.n_tiles;
-            s.mt = t % p.mp_tiles;
+            s.mt = r % p.mp_tiles;
+            s.nt = r / p.mp_tiles;
+        } else if (p.raster == 1) {  // n fastest: concurrent CTAs share the A panel
+            s.nt = r % p.n_tiles;
+            s.mt = r / p.n_tiles;
+        } else if (p.raster == 2) {  // bands of 8 m-tiles, m fastest inside a band, then n
+            const int band = r / (8 * p.n_tiles), rows = min(8, p.mp_tiles - band * 8);
+            r -= band * 8 * p.n_tiles;
+            s.mt = band * 8 + r % rows;
+            s.nt = r / rows;
+        } else {  // bands of 8 n-tiles, n fastest inside a band, then m
+            const int band = r / (8 * p.mp_tiles), cols = min(8, p.n_tiles - band * 8);
+            r -= band * 8 * p.mp_tiles;
+            s.nt = band * 8 + r % cols;
+            s.mt = r / cols;
         }
-        s.bz = t / (p.raster == 0 ? p.n_tiles : p.mp_tiles);
         return true;
     }
 };
@@ -194,11 +208,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 
-template <int BN, int BK, int STAGES, int TQ, int CG>
+template <int BN, int BK, int TQ, int CG>
 __global__ void __launch_bounds__(192, 1)
     tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmY, const TcParams p) {
-    using Cfg = TcCfg<BN, BK, STAGES, CG>;
+    using Cfg = TcCfg<BN, BK, CG>;
+    const int STAGES = p.stages;
     constexpr int BM = Cfg::BM;
     constexpr bool CONV = TQ > 0;
     constexpr int TP = CONV ? BM / TQ : 1;
@@ -597,19 +612,19 @@ static bool encode_f32(CUtensorMap* m, void* ptr, int rank, const cuuint64_t* di
 // shape (it accounts for the ~240 registers per thread of these kernels), capped by TMEM
 // (512 columns per SM) and by the shared-memory bound; never more than one group per CG SMs
 // times that.
-template <int BN, int BK, int STAGES, int TQ, int CG>
-static long long tc_resident_groups(int num_sms, int epi) {
-    using Cfg = TcCfg<BN, BK, STAGES, CG>;
-    static std::atomic<long long> cache[64][2];
+template <int BN, int BK, int TQ, int CG>
+static long long tc_resident_groups(int num_sms, int stages) {
+    using Cfg = TcCfg<BN, BK, CG>;
+    static std::atomic<long long> cache[64][Cfg::MAX_STAGES + 1];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-    long long v = cache[dev & 63][epi - 1].load(std::memory_order_relaxed);
+    long long v = cache[dev & 63][stages].load(std::memory_order_relaxed);
     if (v > 0) return v;
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(CG);
     cfg.blockDim = dim3(Cfg::THREADS);
-    cfg.dynamicSmemBytes = Cfg::smem(epi);
+    cfg.dynamicSmemBytes = Cfg::smem(stages);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
@@ -618,17 +633,17 @@ static long long tc_resident_groups(int num_sms, int epi) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int clusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&clusters, tc_gemm_bf16_kernel<BN, BK, STAGES, TQ, CG>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&clusters, tc_gemm_bf16_kernel<BN, BK, TQ, CG>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         clusters = 0;
     }
-    int per_sm = (int)((228 * 1024) / (Cfg::smem(epi) + 1024));
+    int per_sm = (int)((228 * 1024) / (Cfg::smem(stages) + 1024));
     const int tmem_per_sm = (int)(512 / Cfg::TMEM_COLS);
     per_sm = per_sm < tmem_per_sm ? per_sm : tmem_per_sm;
     per_sm = per_sm < 1 ? 1 : per_sm;
     long long g = (long long)(num_sms / CG) * per_sm;
     if (clusters > 0 && clusters < g) g = clusters;
-    cache[dev & 63][epi - 1].store(g, std::memory_order_relaxed);
+    cache[dev & 63][stages].store(g, std::memory_order_relaxed);
     return g;
 }
 
@@ -641,11 +656,11 @@ static bool make_kmajor_map(CUtensorMap* m, const void* ptr, int64_t batch, int6
     return encode(m, ptr, 3, dims, strides, box, es);
 }
 
-template <int BN, int BK, int STAGES, int TQ, int CG>
+template <int BN, int BK, int TQ, int CG>
 cudaError_t tc_launch(const LaunchCtx& c) {
-    using Cfg = TcCfg<BN, BK, STAGES, CG>;
+    using Cfg = TcCfg<BN, BK, CG>;
     constexpr bool CONV = TQ > 0;
-    auto kern = tc_gemm_bf16_kernel<BN, BK, STAGES, TQ, CG>;
+    auto kern = tc_gemm_bf16_kernel<BN, BK, TQ, CG>;
     static std::atomic<unsigned long long> optin{0};
     {
         cudaError_t e = smem_optin(optin, kern, 227 * 1024);
@@ -726,9 +741,10 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     // persistent grid: as many CTA groups as can be co-resident (the stream-K flag protocol
     // spins heads on their tails, so every group MUST be resident at once): the occupancy
     // calculator's active clusters (registers, shared memory, cluster shape) capped by TMEM
-    const int epi = c.epi == 2 ? 2 : 1;
-    if (Cfg::smem(epi) > 227 * 1024) return cudaErrorInvalidConfiguration;
-    const long long groups_max = tc_resident_groups<BN, BK, STAGES, TQ, CG>(c.num_sms, epi);
+    const int stages = c.stages;
+    if (stages < 2 || stages > Cfg::MAX_STAGES || Cfg::smem(stages) > 227 * 1024) return cudaErrorInvalidConfiguration;
+    p.stages = stages;
+    const long long groups_max = tc_resident_groups<BN, BK, TQ, CG>(c.num_sms, stages);
     if (groups_max < 1) return cudaErrorInvalidConfiguration;
     long long groups = groups_max;
     if (c.sched >= 1) {
@@ -754,7 +770,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     std::memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)(groups * CG));
     cfg.blockDim = dim3(Cfg::THREADS);
-    cfg.dynamicSmemBytes = Cfg::smem(p.epi);
+    cfg.dynamicSmemBytes = Cfg::smem(stages);
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -793,23 +809,21 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-constexpr bool tc_static_ok(int BN, int BK, int STAGES, int CG) {
-    return 1024 + (size_t)STAGES * (128 + BN / CG) * BK * 2 + 256 + kTcEpiBytes <= 227 * 1024;
+constexpr bool tc_static_ok(int BN, int BK, int CG) {  // at least a 2-stage ring fits
+    return 1024 + (size_t)2 * (128 + BN / CG) * BK * 2 + 256 + kTcEpiBytes <= 227 * 1024;
 }
 
-template <int BN, int BK, int STAGES, int TQ, int CG>
-void tc_register() {
-    if constexpr (tc_static_ok(BN, BK, STAGES, CG))
-        registry_add(kernel_key(TQ ? SK_TC_IGEMM_CONV_BF16 : SK_TC_GEMM_BF16, 128 * CG, BN, BK, STAGES, TQ),
-                     &tc_launch<BN, BK, STAGES, TQ, CG>);
+template <int BN, int BK, int TQ, int CG>
+void tc_register() {  // key: (sketch, BM, BN, BK, -, TILE_Q); STAGES is a runtime knob
+    if constexpr (tc_static_ok(BN, BK, CG))
+        registry_add(kernel_key(TQ ? SK_TC_IGEMM_CONV_BF16 : SK_TC_GEMM_BF16, 128 * CG, BN, BK, 0, TQ),
+                     &tc_launch<BN, BK, TQ, CG>);
 }
 
-#define TC_STAGES(BN, BK, TQ, CG)                                                                            \
-    tc_register<BN, BK, 2, TQ, CG>(); tc_register<BN, BK, 3, TQ, CG>(); tc_register<BN, BK, 4, TQ, CG>(); \
-    tc_register<BN, BK, 6, TQ, CG>();
-#define TC_SHAPES(TQ, CG)                                                                        \
-    TC_STAGES(64, 64, TQ, CG) TC_STAGES(128, 64, TQ, CG) TC_STAGES(256, 64, TQ, CG)             \
-    TC_STAGES(64, 128, TQ, CG) TC_STAGES(128, 128, TQ, CG) TC_STAGES(256, 128, TQ, CG)
+#define TC_SHAPES(TQ, CG)                                                                                        \
+    tc_register<64, 64, TQ, CG>(); tc_register<128, 64, TQ, CG>(); tc_register<192, 64, TQ, CG>();             \
+    tc_register<256, 64, TQ, CG>(); tc_register<64, 128, TQ, CG>(); tc_register<128, 128, TQ, CG>();           \
+    tc_register<192, 128, TQ, CG>(); tc_register<256, 128, TQ, CG>();
 
 void register_tc_gemm() {
     TC_SHAPES(0, 1) TC_SHAPES(0, 2)     // dense / bmm

@@ -51,8 +51,11 @@ static std::vector<SketchDesc> build_catalogue() {
     // EPI (runtime): how the epilogue writes the fp32 tile, both staged through 128B-swizzled shared
     // memory: 1 = TMA stores (cp.async.bulk.tensor), 2 = coalesced 128-byte st.global segments.
     const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER", "EPI"};
-    const std::vector<std::vector<int32_t>> tc_vals = {{128, 256}, {64, 128, 256}, {64, 128}, {2, 3, 4, 6},
-                                                       {1, 2, 4},  {0, 1, 2},       {0, 1},    {1, 2}};
+    // STAGES and SPLIT_K are runtime knobs (the ring depth sizes dynamic shared memory).  RASTER:
+    // 0 = M fastest, 1 = N fastest, 2 / 3 = bands of 8 M / N tiles (L2 reuse of both panels).
+    const std::vector<std::vector<int32_t>> tc_vals = {{128, 256}, {64, 128, 192, 256}, {64, 128},
+                                                       {2, 3, 4, 5, 6, 7, 8}, {1, 2, 3, 4, 6, 8}, {0, 1, 2},
+                                                       {0, 1, 2, 3},          {1, 2}};
     c.push_back({SK_TC_GEMM_BF16, "tc_gemm_bf16", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL), TUNER_BF16,
                  tc_names, tc_vals});
     // implicit-GEMM conv: the 128-row M tile is a (128/TILE_Q) x TILE_Q rectangle of output pixels
@@ -61,7 +64,7 @@ static std::vector<SketchDesc> build_catalogue() {
     std::vector<std::vector<int32_t>> tcc_vals(tc_vals.begin(), tc_vals.end() - 3);
     tcc_vals.push_back({8, 16, 32});
     tcc_vals.push_back({0, 1, 2});
-    tcc_vals.push_back({0, 1});
+    tcc_vals.push_back({0, 1, 2, 3});
     tcc_vals.push_back({1, 2});
     c.push_back({SK_TC_IGEMM_CONV_BF16, "tc_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tcc_names,
                  tcc_vals});

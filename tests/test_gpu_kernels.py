@@ -236,8 +236,14 @@ def test_tc_gemm_all_configs_vs_oracle(shape):
     t = Tuner(op, {"b": b, "m": m, "n": n, "k": k}, dtype="bf16", spaces=[(2, sketch_space(2))], x=xd, w=wd, y=y)
     pts = [p for p in all_points(2) if t.valid(p)]
     assert len(pts) >= 10
+    # every compiled (BM, BN, BK) instantiation, with a sample of the runtime knobs over it
+    rng = random.Random(sum(shape))
+    by_inst = {}
+    for p in pts:
+        by_inst.setdefault(tuple(p[1][:3]), []).append(p)
+    sel = [q for group in by_inst.values() for q in rng.sample(group, min(len(group), 40))]
     bad, worst = [], 0.0
-    for p, yv in run_points(t, pts, xd, wd, y):
+    for p, yv in run_points(t, sel, xd, wd, y):
         e = on.max_rel_err(yv.reshape(yo.shape), yo, ao)
         worst = max(worst, e)
         if not e <= 1e-5:  # fp32 accumulation of exact bf16 products: far inside the 2e-2 bar
@@ -252,7 +258,7 @@ def test_tc_gemm_exact_integer_inputs():
     y = torch.empty(b, m, n, device=dev())
     t = Tuner("dense", {"m": m, "n": n, "k": k}, dtype="bf16", spaces=[(2, sketch_space(2))], x=xd, w=wd, y=y)
     pts = [p for p in all_points(2) if t.valid(p)]
-    for p, yv in run_points(t, pts, xd, wd, y):
+    for p, yv in run_points(t, random.Random(3).sample(pts, min(400, len(pts))), xd, wd, y):
         np.testing.assert_array_equal(yv.reshape(yo.shape), yo.astype(np.float32), err_msg=str(t.values(p)))
 
 

@@ -40,9 +40,17 @@ def case_tensors(case, dist):
     return shape, xd, wd, yo, ao
 
 
-def points(t):
+def points(t, per_instance=40, seed=0):
+    """Every compiled (BM, BN, BK, TILE_Q) instantiation valid for the shape, each with a sample of
+    its runtime knobs (STAGES, SPLIT_K, SCHED, RASTER, EPI)."""
+    import random
     vals = sketch_space(SK)
-    return [(SK, idx) for idx in itertools.product(*[range(len(v)) for v in vals]) if t.valid((SK, idx))]
+    pts = [(SK, idx) for idx in itertools.product(*[range(len(v)) for v in vals]) if t.valid((SK, idx))]
+    by_inst = {}
+    for p in pts:
+        by_inst.setdefault((p[1][0], p[1][1], p[1][2], p[1][5]), []).append(p)
+    rng = random.Random(seed)
+    return [q for g in by_inst.values() for q in rng.sample(g, min(len(g), per_instance))]
 
 
 @pytest.mark.parametrize("case", CASES)
