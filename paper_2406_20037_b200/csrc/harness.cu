@@ -166,22 +166,22 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
             rk.red = v[9];
             rk.cluster = v[9] == 1 ? v[7] : 1;
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[3], v[4] | (v[5] << 4)));
-        case SK_TC_GEMM_BF16:  // BM, BN, BK (compiled) | STAGES, SPLIT_K, SCHED, RASTER, EPI
+        case SK_TC_GEMM_BF16:  // BM, BN, BK, EW (compiled) | STAGES, SPLIT_K, SCHED, RASTER, EPI
             rk.stages = v[3];
             rk.split = v[4];
             rk.sched = v[5];
             rk.raster = v[6];
             rk.epi = v[7];
             rk.cluster = v[0] / 128;
-            return registry_find(kernel_key(sk, v[0], v[1], v[2], 0, 0));
-        case SK_TC_IGEMM_CONV_BF16:  // BM, BN, BK, TILE_Q (compiled) | STAGES, SPLIT_K, SCHED, RASTER, EPI
+            return registry_find(kernel_key(sk, v[0], v[1], v[2], v[8], 0));
+        case SK_TC_IGEMM_CONV_BF16:  // BM, BN, BK, TILE_Q, EW (compiled) | STAGES, SPLIT_K, SCHED, RASTER, EPI
             rk.stages = v[3];
             rk.split = v[4];
             rk.sched = v[6];
             rk.raster = v[7];
             rk.epi = v[8];
             rk.cluster = v[0] / 128;
-            return registry_find(kernel_key(sk, v[0], v[1], v[2], 0, v[5]));
+            return registry_find(kernel_key(sk, v[0], v[1], v[2], v[9], v[5]));
         case SK_SIMT_DIRECT_CONV_F32:  // KT, TP (compiled) | PX, BKC, EPI
         case SK_SIMT_DIRECT_CONV_BF16:
             rk.dims[0] = v[2];

@@ -43,8 +43,10 @@
 namespace db200 {
 
 
-// STAGES is a runtime knob (the ring depth only sizes shared memory and indexes the ring)
-template <int BN, int BK, int CG>
+// STAGES is a runtime knob (the ring depth only sizes shared memory and indexes the ring).
+// EW = epilogue warps: 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each draining every
+// other 32-column chunk: twice the TMA stores in flight per SM)
+template <int BN, int BK, int CG, int EW = 4>
 struct TcCfg {
     static constexpr int BM = 128;  // rows of A per CTA
     static constexpr int BNC = BN / CG;  // rows of B per CTA
@@ -65,7 +67,9 @@ struct TcCfg {
     static_assert(EPI_BYTES == kTcEpiBytes, "epilogue staging size");
     static constexpr int MAX_STAGES = 8;
     static constexpr size_t smem(int stages) { return 1024 + (size_t)stages * STAGE_BYTES + (size_t)EPI_BYTES + 256; }
-    static constexpr int THREADS = 192;
+    static constexpr int THREADS = 64 + 32 * EW;
+    static constexpr int CH = EW == 4 ? (BN < 64 ? BN : 64) : 32;  // columns per TMEM drain and staging
+    static constexpr int CSTEP = CH * (EW / 4);                   // column stride between a warp's chunks
 };
 
 struct TcParams {
@@ -206,13 +210,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
         if (p.trace) p.trace[(size_t)blockIdx.x * 16 + (slot)] = gtimer();               \
     } while (0)
 
-__device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void epi_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
-template <int BN, int BK, int TQ, int CG>
-__global__ void __launch_bounds__(192, 1)
+template <int BN, int BK, int TQ, int CG, int EW>
+__global__ void __launch_bounds__(64 + 32 * EW, 1)
     tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmY, const TcParams p) {
-    using Cfg = TcCfg<BN, BK, CG>;
+    using Cfg = TcCfg<BN, BK, CG, EW>;
     const int STAGES = p.stages;
     constexpr int BM = Cfg::BM;
     constexpr bool CONV = TQ > 0;
@@ -239,7 +245,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(tc::smem_u32(&acc_full[a]), 1);
-            tc::mbar_init(tc::smem_u32(&acc_empty[a]), 4 * CG);  // one arrive per epilogue warp of the group
+            tc::mbar_init(tc::smem_u32(&acc_empty[a]), EW * CG);  // one arrive per epilogue warp of the group
         }
         tc::fence_barrier_init();
         tc::tma_prefetch(&tmA);
@@ -352,7 +358,9 @@ __global__ void __launch_bounds__(192, 1)
         }
     } else {  // ---- epilogue: TMEM -> registers -> global
         if (p.split > 1) griddep_wait();  // split-K: Y zeroed by the prerequisite grid (PDL)
-        const int q = warp & 3;
+        const int q = warp & 3;          // TMEM lane quadrant this warp may access (warp % 4)
+        const int ew = warp - 2;         // epilogue warp index 0..EW-1
+        const int half = ew >> 2;        // EW = 8: which of the quadrant's two warps (chunk parity)
         const int trow = q * 32 + lane;  // row of the 128-row sub-tile held by this thread
         const bool vec_ok = (p.N % 4) == 0;  // TMA needs 16-byte global strides
         int j = 0;
@@ -403,7 +411,7 @@ __global__ void __launch_bounds__(192, 1)
                     }
                     TC_TRACE(9);
                 }
-                epi_bar(1);
+                epi_bar(1, 32 * EW);
             }
             const bool red = w.mode == EPI_RED;
             // a parked partial is stored thread-major, [BN/16][128 rows][16], so each warp
@@ -413,9 +421,9 @@ __global__ void __launch_bounds__(192, 1)
             const int n0 = w.mode == EPI_TAIL ? 0 : w.nt * BN;
             const bool live = w.mode == EPI_TAIL ? true : row_ok;
             const int ncols = w.mode == EPI_TAIL ? BN : p.N;
-            constexpr int CH = BN < 64 ? BN : 64;  // columns per TMEM drain: several loads, one wait
+            constexpr int CH = Cfg::CH;  // columns per TMEM drain: several loads, one wait
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += CH) {
+            for (int c0 = half * CH; c0 < BN; c0 += Cfg::CSTEP) {
                 uint32_t r[CH / 16][16];
 #pragma unroll
                 for (int g = 0; g < CH / 16; ++g)
@@ -449,7 +457,7 @@ __global__ void __launch_bounds__(192, 1)
                     // columns, lane = box row, 16-byte chunk c of a row at physical chunk
                     // c ^ (row & 7) (SWIZZLE_128B: conflict-free st.shared.v4 / ld.shared.v4)
                     static_assert(CH % 32 == 0, "staged chunks are 32 columns wide");
-                    const uint32_t eb = tc::smem_u32(epi_smem + q * (2 * Cfg::EPI_BOX));
+                    const uint32_t eb = tc::smem_u32(epi_smem + ew * (CH / 32) * Cfg::EPI_BOX);
                     if (p.epi == 1) {
                         if (lane == 0) tc::bulk_wait_read<0>();  // the previous chunk's stores have read it
                         __syncwarp();
@@ -543,13 +551,13 @@ __global__ void __launch_bounds__(192, 1)
             }
             if (warp == 2 && lane == 0 && j < 4) TC_TRACE(5 + j);
             if (w.mode == EPI_TAIL) {  // publish the parked partial (flag = 1)
-                epi_bar(2);
+                epi_bar(2, 32 * EW);
                 if (warp == 2 && lane == 0) {
                     __threadfence();
                     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.flags + slot), "r"(1u) : "memory");
                 }
             } else if (w.mode == EPI_HEAD) {  // partials consumed: re-arm the tails' flags (0)
-                epi_bar(2);
+                epi_bar(2, 32 * EW);
                 if (warp == 2 && lane == 0) {
                     for (int tl = 1; tl <= w.ntails; ++tl) p.flags[slot + tl * w.tstride * CG] = 0u;
                 }
@@ -612,9 +620,9 @@ static bool encode_f32(CUtensorMap* m, void* ptr, int rank, const cuuint64_t* di
 // shape (it accounts for the ~240 registers per thread of these kernels), capped by TMEM
 // (512 columns per SM) and by the shared-memory bound; never more than one group per CG SMs
 // times that.
-template <int BN, int BK, int TQ, int CG>
+template <int BN, int BK, int TQ, int CG, int EW>
 static long long tc_resident_groups(int num_sms, int stages) {
-    using Cfg = TcCfg<BN, BK, CG>;
+    using Cfg = TcCfg<BN, BK, CG, EW>;
     static std::atomic<long long> cache[64][Cfg::MAX_STAGES + 1];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
@@ -633,7 +641,7 @@ static long long tc_resident_groups(int num_sms, int stages) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int clusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&clusters, tc_gemm_bf16_kernel<BN, BK, TQ, CG>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&clusters, tc_gemm_bf16_kernel<BN, BK, TQ, CG, EW>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         clusters = 0;
     }
@@ -656,11 +664,11 @@ static bool make_kmajor_map(CUtensorMap* m, const void* ptr, int64_t batch, int6
     return encode(m, ptr, 3, dims, strides, box, es);
 }
 
-template <int BN, int BK, int TQ, int CG>
+template <int BN, int BK, int TQ, int CG, int EW>
 cudaError_t tc_launch(const LaunchCtx& c) {
-    using Cfg = TcCfg<BN, BK, CG>;
+    using Cfg = TcCfg<BN, BK, CG, EW>;
     constexpr bool CONV = TQ > 0;
-    auto kern = tc_gemm_bf16_kernel<BN, BK, TQ, CG>;
+    auto kern = tc_gemm_bf16_kernel<BN, BK, TQ, CG, EW>;
     static std::atomic<unsigned long long> optin{0};
     {
         cudaError_t e = smem_optin(optin, kern, 227 * 1024);
@@ -744,7 +752,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     const int stages = c.stages;
     if (stages < 2 || stages > Cfg::MAX_STAGES || Cfg::smem(stages) > 227 * 1024) return cudaErrorInvalidConfiguration;
     p.stages = stages;
-    const long long groups_max = tc_resident_groups<BN, BK, TQ, CG>(c.num_sms, stages);
+    const long long groups_max = tc_resident_groups<BN, BK, TQ, CG, EW>(c.num_sms, stages);
     if (groups_max < 1) return cudaErrorInvalidConfiguration;
     long long groups = groups_max;
     if (c.sched >= 1) {
@@ -814,10 +822,13 @@ constexpr bool tc_static_ok(int BN, int BK, int CG) {  // at least a 2-stage rin
 }
 
 template <int BN, int BK, int TQ, int CG>
-void tc_register() {  // key: (sketch, BM, BN, BK, -, TILE_Q); STAGES is a runtime knob
-    if constexpr (tc_static_ok(BN, BK, CG))
-        registry_add(kernel_key(TQ ? SK_TC_IGEMM_CONV_BF16 : SK_TC_GEMM_BF16, 128 * CG, BN, BK, 0, TQ),
-                     &tc_launch<BN, BK, TQ, CG>);
+void tc_register() {  // key: (sketch, BM, BN, BK, EW, TILE_Q); STAGES is a runtime knob
+    if constexpr (tc_static_ok(BN, BK, CG)) {
+        registry_add(kernel_key(TQ ? SK_TC_IGEMM_CONV_BF16 : SK_TC_GEMM_BF16, 128 * CG, BN, BK, 4, TQ),
+                     &tc_launch<BN, BK, TQ, CG, 4>);
+        registry_add(kernel_key(TQ ? SK_TC_IGEMM_CONV_BF16 : SK_TC_GEMM_BF16, 128 * CG, BN, BK, 8, TQ),
+                     &tc_launch<BN, BK, TQ, CG, 8>);
+    }
 }
 
 #define TC_SHAPES(TQ, CG)                                                                                        \

@@ -50,22 +50,25 @@ static std::vector<SketchDesc> build_catalogue() {
     // (concurrent CTAs share the B panel), 1 = N fastest (they share the A panel).
     // EPI (runtime): how the epilogue writes the fp32 tile, both staged through 128B-swizzled shared
     // memory: 1 = TMA stores (cp.async.bulk.tensor), 2 = coalesced 128-byte st.global segments.
-    const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER", "EPI"};
+    // EW (compiled): epilogue warps, 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each
+    // draining every other 32-column chunk).
+    const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER", "EPI", "EW"};
     // STAGES and SPLIT_K are runtime knobs (the ring depth sizes dynamic shared memory).  RASTER:
     // 0 = M fastest, 1 = N fastest, 2 / 3 = bands of 8 M / N tiles (L2 reuse of both panels).
     const std::vector<std::vector<int32_t>> tc_vals = {{128, 256}, {64, 128, 192, 256}, {64, 128},
                                                        {2, 3, 4, 5, 6, 7, 8}, {1, 2, 3, 4, 6, 8}, {0, 1, 2},
-                                                       {0, 1, 2, 3},          {1, 2}};
+                                                       {0, 1, 2, 3},          {1, 2},       {4, 8}};
     c.push_back({SK_TC_GEMM_BF16, "tc_gemm_bf16", (1 << TUNER_OP_DENSE) | (1 << TUNER_OP_BATCH_MATMUL), TUNER_BF16,
                  tc_names, tc_vals});
     // implicit-GEMM conv: the 128-row M tile is a (128/TILE_Q) x TILE_Q rectangle of output pixels
     const std::vector<const char*> tcc_names = {"BM",     "BN",    "BK",     "STAGES", "SPLIT_K",
-                                                "TILE_Q", "SCHED", "RASTER", "EPI"};
-    std::vector<std::vector<int32_t>> tcc_vals(tc_vals.begin(), tc_vals.end() - 3);
+                                                "TILE_Q", "SCHED", "RASTER", "EPI",    "EW"};
+    std::vector<std::vector<int32_t>> tcc_vals(tc_vals.begin(), tc_vals.end() - 4);
     tcc_vals.push_back({8, 16, 32});
     tcc_vals.push_back({0, 1, 2});
     tcc_vals.push_back({0, 1, 2, 3});
     tcc_vals.push_back({1, 2});
+    tcc_vals.push_back({4, 8});
     c.push_back({SK_TC_IGEMM_CONV_BF16, "tc_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tcc_names,
                  tcc_vals});
     // the SIMT implicit-GEMM sketch on bf16 inputs (widened to fp32 at staging, fp32

@@ -49,8 +49,8 @@ def test_catalogue():
     assert knob_names(0) == ["BM", "BN", "BK", "TT", "UNROLL", "VEC", "STAGES", "SPLIT_K"]
     sp = sketch_space(0)
     assert sp[0] == [16, 32, 64, 128] and sp[7] == [1, 2, 3, 4, 6, 8, 12, 16]
-    assert knob_names(2) == ["BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER", "EPI"]
-    assert knob_names(3) == ["BM", "BN", "BK", "STAGES", "SPLIT_K", "TILE_Q", "SCHED", "RASTER", "EPI"]
+    assert knob_names(2) == ["BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER", "EPI", "EW"]
+    assert knob_names(3) == ["BM", "BN", "BK", "STAGES", "SPLIT_K", "TILE_Q", "SCHED", "RASTER", "EPI", "EW"]
     assert sketch_name(8) == "simt_pipe_conv_f32"
     assert knob_names(8) == ["BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K", "OCC", "RED"]
     assert sketch_name(10) == "simt_direct_conv_bf16"

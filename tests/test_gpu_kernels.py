@@ -240,7 +240,7 @@ def test_tc_gemm_all_configs_vs_oracle(shape):
     rng = random.Random(sum(shape))
     by_inst = {}
     for p in pts:
-        by_inst.setdefault(tuple(p[1][:3]), []).append(p)
+        by_inst.setdefault(tuple(p[1][:3]) + (p[1][8],), []).append(p)
     sel = [q for group in by_inst.values() for q in rng.sample(group, min(len(group), 40))]
     bad, worst = [], 0.0
     for p, yv in run_points(t, sel, xd, wd, y):

@@ -77,7 +77,7 @@ def test_c3_layers_have_a_bf16_schedule(L):
     P, Q = out_hw(L)
     y = torch.empty((L["N"], P, Q, L["K"]), device="cuda:0")
     t = Tuner("conv2d", shape, dtype="bf16", x=xd, w=wd, y=y, seed=0, early_cut=4.0)
-    assert not any(t.valid((3, p)) for p in [(0, 0, 0, 0, 0, 0, 0, 0, 0), (1, 1, 0, 1, 0, 1, 0, 1, 1)])
+    assert not any(t.valid((3, p)) for p in [(0, 0, 0, 0, 0, 0, 0, 0, 0, 0), (1, 1, 0, 1, 0, 1, 0, 1, 1, 1)])
     smp = t.evolve(40, pop=16, elite=4)
     assert smp and all(s.status == "ok" and s.point[0] in (SK, 10) for s in smp)  # SIMT igemm or direct
     rep = t.droplet(t.best().point, 40)

@@ -48,7 +48,7 @@ def points(t, per_instance=40, seed=0):
     pts = [(SK, idx) for idx in itertools.product(*[range(len(v)) for v in vals]) if t.valid((SK, idx))]
     by_inst = {}
     for p in pts:
-        by_inst.setdefault((p[1][0], p[1][1], p[1][2], p[1][5]), []).append(p)
+        by_inst.setdefault((p[1][0], p[1][1], p[1][2], p[1][5], p[1][9]), []).append(p)
     rng = random.Random(seed)
     return [q for g in by_inst.values() for q in rng.sample(g, min(len(g), per_instance))]
 
