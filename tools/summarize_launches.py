@@ -10,7 +10,7 @@ import sys
 
 
 def family(name):
-    for key in ("simt_gemm_f32_kernel", "simt_pipe_kernel", "direct_conv_kernel", "zero_splitk", "tc_gemm_bf16_kernel", "tc_conv_bf16_kernel", "verify_maxerr",
+    for key in ("simt_gemm_f32_kernel", "simt_pipe_kernel", "direct_conv_kernel", "zero_splitk", "tc_gemm_bf16_kernel", "tc_conv_bf16_kernel", "verify_maxerr", "fp32_peak_kernel",
                 "naive_ref_conv", "naive_ref_gemm"):
         if key in name:
             return key
