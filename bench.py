@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--droplet-sketch-factor", type=float, default=1.5,
                     help="Droplet also starts from the best point of every other sketch within this factor "
                          "of the overall best (R-D17); 1.0 = the paper's single start")
+    ap.add_argument("--droplet-policy", default="grow", choices=["plain", "grow", "radius"],
+                    help="Droplet step rule: plain (the paper's text), grow (R-D9), radius (R-D16)")
     ap.add_argument("--baseline", type=int, default=10000)
     ap.add_argument("--early-cut", type=float, default=4.0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -321,7 +323,7 @@ def main():
         # DPAnsor: explore N, best-of-N, Droplet to convergence (<= 100 trials)
         t0 = time.perf_counter()
         tu = Tuner(L["op"], shape_of(L), dtype=dt, spaces=sp, x=xd, w=wd, y=y, seed=seed, group=group,
-                   stream=stream, early_cut=args.early_cut)
+                   stream=stream, early_cut=args.early_cut, policy=args.droplet_policy)
         smp = tu.evolve(args.n_sample) if args.explore == "evolve" else tu.sample(args.n_sample)
         if not smp:  # no compiled sketch covers this layer (e.g. bf16 TMA needs C % 8 == 0)
             tu.close()

@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdroplet_b200.so")
+# DB200_LIB: another build of the same library (A/B experiments under tools/ only)
+LIB_PATH = os.environ.get("DB200_LIB") or os.path.join(_HERE, "lib", "libdroplet_b200.so")
 
 MAX_KNOBS = 16
 MAX_VALUES = 64

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
     constexpr int STAGE_FLOATS = (BM + BN) * LDK;
     const size_t pipe_floats = (size_t)stages * STAGE_FLOATS;
     const bool staged_epi = KW > 1 || p.split > 1;  // epilogue through shared memory
-    const size_t red_floats = staged_epi ? (size_t)KW * BM * BN : 0;
+    const size_t red_floats = staged_epi ? (size_t)KW * BM * pipe_red_ld(BN) : 0;
     // one-unit CTAs stage the epilogue tile over the drained ring; persistent CTAs keep the
     // next unit's tiles in flight during an epilogue, so their tile has its own region
     float* red = p.persist ? smem + pipe_floats : smem;
@@ -101,7 +101,23 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
 
     const int tid = threadIdx.x;
     const int g = tid / GT, gt = tid % GT;
-    const int tx = gt % TX, ty = gt / TX;
+    // a warp covers an 8 x 4 (or 4 x 8) patch of the thread grid: its fragment loads touch 8
+    // B rows and 4 A rows (4 and 8), one 128-byte shared-memory wavefront each, where a
+    // 16 x 2 or 32 x 1 patch needs 2-4 wavefronts per B load
+    int tx, ty;
+    if constexpr (TX % 8 == 0 && TY % 4 == 0) {
+        const int lane = gt & 31, wi = gt >> 5;
+        tx = (wi % (TX / 8)) * 8 + (lane & 7);
+        ty = (wi / (TX / 8)) * 4 + (lane >> 3);
+    } else if constexpr (TX % 4 == 0 && TY % 8 == 0) {
+        const int lane = gt & 31, wi = gt >> 5;
+        tx = (wi % (TX / 4)) * 4 + (lane & 3);
+        ty = (wi / (TX / 4)) * 8 + (lane >> 2);
+    } else {
+        tx = gt % TX;
+        ty = gt / TX;
+    }
+    constexpr int RLD = pipe_red_ld(BN);  // staged epilogue tile row stride (floats)
     constexpr int CPR = BK / VW;  // cp.async chunks per tile row
     const int u0 = blockIdx.x, ustep = gridDim.x;
     // programmatic dependent launch: the next kernel in the stream may start its own prologue now
@@ -284,17 +300,18 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
         for (int i = 0; i < TT; ++i)
 #pragma unroll
             for (int j = 0; j < TT; ++j)
-                red[(g * BM + ty + i * TY) * BN + tx + j * TX] = acc[i][j].x + acc[i][j].y;
+                red[(g * BM + ty + i * TY) * RLD + tx + j * TX] = acc[i][j].x + acc[i][j].y;
         if constexpr (KW > 1) {
             __syncthreads();
             for (int e = tid; e < BM * BN / 4; e += NT) {
-                float4 v = reinterpret_cast<const float4*>(red)[e];
+                const int o = (e / (BN / 4)) * RLD + (e % (BN / 4)) * 4;
+                float4 v = *reinterpret_cast<const float4*>(red + o);
 #pragma unroll
                 for (int q = 1; q < KW; ++q) {
-                    const float4 u = reinterpret_cast<const float4*>(red + q * BM * BN)[e];
+                    const float4 u = *reinterpret_cast<const float4*>(red + q * BM * RLD + o);
                     v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
                 }
-                reinterpret_cast<float4*>(red)[e] = v;
+                *reinterpret_cast<float4*>(red + o) = v;
             }
         }
         cluster_barrier();  // every CTA's partial tile is in its shared memory
@@ -309,7 +326,7 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int q = 0; q < S; ++q) {
                 uint32_t ra;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(red_s + (uint32_t)e * 16u), "r"(q));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(red_s + (uint32_t)(row * RLD + col) * 4u), "r"(q));
                 float4 u;
                 asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
                              : "=f"(u.x), "=f"(u.y), "=f"(u.z), "=f"(u.w) : "r"(ra) : "memory");
@@ -357,17 +374,17 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
         for (int i = 0; i < TT; ++i)
 #pragma unroll
             for (int j = 0; j < TT; ++j)
-                red[(g * BM + ty + i * TY) * BN + tx + j * TX] = acc[i][j].x + acc[i][j].y;
+                red[(g * BM + ty + i * TY) * RLD + tx + j * TX] = acc[i][j].x + acc[i][j].y;
         __syncthreads();
         const bool vec_ok = (p.N % 4) == 0;
         for (int e = tid; e < BM * BN / 4; e += NT) {
             const int row = e / (BN / 4), col = (e % (BN / 4)) * 4;
             const int m = w.m0 + row, n = w.n0 + col;
             if (m >= p.M) continue;
-            float4 v = *reinterpret_cast<const float4*>(red + row * BN + col);
+            float4 v = *reinterpret_cast<const float4*>(red + row * RLD + col);
 #pragma unroll
             for (int q = 1; q < KW; ++q) {
-                const float4 u = *reinterpret_cast<const float4*>(red + (q * BM + row) * BN + col);
+                const float4 u = *reinterpret_cast<const float4*>(red + (q * BM + row) * RLD + col);
                 v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
             }
             float* cp = C + (long long)m * p.N + n;

@@ -39,10 +39,13 @@ constexpr bool dw_win_fits(int vec, int tq, int tp, int ks, int sh) {
 // [BM+BN][BK+4] fp32 tiles, or the reduction tile if larger -- KW group partials, or the
 // split-K tile staged for 128-bit atomics -- + the conv k table)
 // (persistent CTAs: ring + reduction tile side by side, the k table over all of K)
+// row stride (floats) of the staged epilogue tile: 8 pad floats put the 4 rows of a warp's
+// 8 x 4 thread patch on disjoint banks
+constexpr int pipe_red_ld(int bn) { return bn + 8; }
 inline size_t pipe_smem_bytes(int bm, int bn, int bk, int kw, int stages, bool conv, int kspan, int vw,
                               int split, int persist = 0) {
     const size_t pipe = (size_t)stages * (bm + bn) * (bk + 4) * 4;
-    const size_t red = (kw > 1 || split > 1) ? (size_t)kw * bm * bn * 4 : 0;
+    const size_t red = (kw > 1 || split > 1) ? (size_t)kw * bm * pipe_red_ld(bn) * 4 : 0;
     const size_t ktab = conv ? (size_t)((kspan + vw - 1) / vw) * 8 : 0;
     return (persist ? pipe + red : (pipe > red ? pipe : red)) + ktab;
 }

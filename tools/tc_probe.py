@@ -44,19 +44,6 @@ def main():
             rep = t.droplet(t.best().point, 60)
             print(f"{mnk:16s} DPAnsor best {t.values(rep['best'])} {rep['best_cost'] / 1e3:9.1f} us "
                   f"{fl / rep['best_cost'] / 1e3:7.1f} TFLOP/s")
-        # torch (cuBLAS) for context
-        xa, wa = x[0], w[0]
-        for _ in range(3):
-            torch.matmul(xa, wa.t())
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(20):
-            torch.matmul(xa, wa.t())
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 20
-        print(f"{mnk:16s} cuBLAS (bf16 out) {ms * 1e3:9.1f} us {fl / ms / 1e9:7.1f} TFLOP/s")
         t.close()
 
 
