@@ -548,7 +548,9 @@ def main():
         "config": {"workload": f"{args.workload} layers ({dtype}): {args.n_sample} samples + Droplet "
                                f"(<= {args.droplet_budget}) vs {args.baseline}-trial random baseline, one layer per step",
                    "l2": "flushed between steps (256 MB write); candidate timings hot-L2 (back-to-back launches)",
-                   "early_cut": args.early_cut, "parallelism": f"candidates sharded x{world}"},
+                   "early_cut": args.early_cut, "droplet_policy": args.droplet_policy,
+                   "droplet_sketch_factor": args.droplet_sketch_factor,
+                   "parallelism": f"candidates sharded x{world}"},
         "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu_baseline,
         "tuning_wall_s": {"dpansor": round(dp_wall, 3), "baseline_10k": round(bl_wall, 3),
                           "speedup": round(bl_wall / dp_wall, 2) if dp_wall > 0 else None},

@@ -215,6 +215,13 @@ void tuner_opts_default(tuner_opts* o);
  *   5 simt_dwconv_f32 / 6 simt_dwconv_bf16      depthwise conv */
 tuner_status tuner_sketches(int32_t op, int32_t dtype, int32_t* ids, int32_t cap, int32_t* n_out);
 tuner_status tuner_sketch_space(int32_t sketch, int32_t* nknobs, int32_t* card, int32_t* values);
+/* The static validity rule of a sketch ("sketch rules are hardware-dependent"; P:596-599
+ * schedules exceeding the hardware's limits are invalid) for one point given by its knob VALUES
+ * (not indices; nvalues = the sketch's knob count) on a problem shape, without a tuner handle
+ * and without a device: the rule tuner_point_valid applies in measured mode.  *valid = 0/1.
+ * EINVAL on a NULL pointer or a bad shape, ERANGE on an unknown sketch, EDIM on a wrong count. */
+tuner_status tuner_sketch_valid(int32_t op, const tuner_shape* shape, int32_t sketch, const int32_t* values,
+                                int32_t nvalues, int32_t* valid);
 const char* tuner_sketch_name(int32_t sketch);
 const char* tuner_knob_name(int32_t sketch, int32_t knob);
 

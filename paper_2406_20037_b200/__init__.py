@@ -3,7 +3,7 @@ as a Raindrop" (arXiv 2406.20037): measuring candidate kernel schedules for
 Ansor-style sampling + Droplet Search, behind the C ABI in include/tuner.h.
 """
 from .tuner import (Sample, Tuner, global_launch_count, knob_names, probe_fp32_peak, rank_sum_p, schedule, sketch_name,  # noqa: F401
-                    sketch_space, sketches)
+                    sketch_space, sketch_valid, sketches)
 from ._lib import LIB_PATH, TunerError  # noqa: F401
 
 SK_SIMT_GEMM_F32 = 0

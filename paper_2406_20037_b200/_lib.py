@@ -80,6 +80,8 @@ SIGNATURES = {
     "tuner_opts_default": (None, [C.POINTER(Opts)]),
     "tuner_sketches": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]),
     "tuner_sketch_space": (C.c_int, [C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "tuner_sketch_valid": (C.c_int, [C.c_int32, C.POINTER(Shape), C.c_int32, C.POINTER(C.c_int32), C.c_int32,
+                                     C.POINTER(C.c_int32)]),
     "tuner_sketch_name": (C.c_char_p, [C.c_int32]),
     "tuner_knob_name": (C.c_char_p, [C.c_int32, C.c_int32]),
     "tuner_create": (C.c_int, [C.c_int32, C.POINTER(Shape), C.POINTER(KnobSpace), C.c_int32, C.POINTER(Opts),

@@ -35,10 +35,17 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
 #include "tc_common.cuh"
+
+// the halo instantiations return from the producer / MMA segment loops before the generic k-block
+// loops (if constexpr + continue): those are dead code there, by design
+#pragma nv_diag_suppress 128
 
 namespace db200 {
 
@@ -93,6 +100,11 @@ struct TcParams {
     int P, Q, S, CB;  // CB = channel blocks of BK per tap
     int sh, sw, ph, pw, dh, dw;
     int tiles_p, tiles_q;
+    // halo tiles (TILE_Q = 128): R input-row windows of 128 + S - 1 pixels per channel block,
+    // each win_bytes apart (1024-aligned), a_stage_bytes = R * win_bytes per A-ring stage
+    int R, win_bytes, a_stage_bytes;
+    int N_img;       // conv: images (a sub-tile with image >= N_img is padding)
+    int contiguous;  // SCHED 0 with contiguous unit ranges per group (halo: runs down the rows)
 };
 
 // epilogue modes of a segment: plain store; split-K reduction into a zeroed Y;
@@ -116,7 +128,10 @@ struct SegIter {
     int u;
     __device__ SegIter(const TcParams& p, int g, int G) {
         u = g;
-        if (p.sched == 2) {  // the remainder unit of this group (if any): [g, g + 1)
+        if (p.contiguous) {  // group g takes units [g U / G, (g+1) U / G) in order
+            cur = (long long)g * p.units / G;
+            end = (long long)(g + 1) * p.units / G;
+        } else if (p.sched == 2) {  // the remainder unit of this group (if any): [g, g + 1)
             cur = g;
             end = g + 1;
         } else {
@@ -126,7 +141,14 @@ struct SegIter {
     }
     __device__ bool next(const TcParams& p, int G, Seg& s) {
         int t;
-        if (p.sched == 0) {
+        if (p.contiguous) {
+            if (cur >= end) return false;
+            t = (int)cur++;
+            s.kb0 = 0;
+            s.nkb = p.kblocks;
+            s.mode = EPI_STORE;
+            s.ntails = 0;
+        } else if (p.sched == 0) {
             if (u >= p.units) return false;
             const int kz = u % p.split;
             t = u / p.split;
@@ -204,7 +226,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 // trace slots: 0 start, 1..4 epilogue segment j ready (acc_full), 5..8 segment j done,
-// 9 head flags seen, 10 end
+// 9 head flags seen, 10 end; halo: 11 / 12 MMA at segment 1 / 2 (accumulator free), 13 segment 2
+// windows landed, 14 producer issued segment 2 windows, 15 MMA issued segment 2
 #define TC_TRACE(slot)                                                                   \
     do {                                                                                 \
         if (p.trace) p.trace[(size_t)blockIdx.x * 16 + (slot)] = gtimer();               \
@@ -222,16 +245,27 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     const int STAGES = p.stages;
     constexpr int BM = Cfg::BM;
     constexpr bool CONV = TQ > 0;
+    constexpr bool HALO = TQ == 128;  // halo row tiles: A staged once per channel block, taps = shifted views
     constexpr int TP = CONV ? BM / TQ : 1;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(base + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES);
+    // shared memory:
+    //   generic: [STAGES x (A slice + B slice of one k-block)][epilogue staging][barriers]
+    //   halo:    [NW = STAGES window slots of CB x (128 + S - 1) input pixels][B resident: all CB x R*S
+    //             taps of the n-tile][epilogue staging][barriers]
+    uint8_t* aring = base;
+    uint8_t* ring = base + (HALO ? STAGES * p.a_stage_bytes : 0);
+    const int ring_bytes = HALO ? p.CB * p.R * p.S * Cfg::B_BYTES : STAGES * Cfg::STAGE_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + ring_bytes + Cfg::EPI_BYTES);
+    const int NB = HALO ? 1 : STAGES;  // halo: one full / empty pair guards the resident B
     uint64_t* full = bars;
-    uint64_t* empty = bars + STAGES;
-    uint64_t* acc_full = bars + 2 * STAGES;       // [2] MMA -> epilogue
-    uint64_t* acc_empty = bars + 2 * STAGES + 2;  // [2] epilogue -> MMA
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
-    float* epi_smem = reinterpret_cast<float*>(base + STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty = bars + NB;
+    uint64_t* acc_full = bars + 2 * NB;       // [2] MMA -> epilogue
+    uint64_t* acc_empty = bars + 2 * NB + 2;  // [2] epilogue -> MMA
+    uint64_t* full_w = bars + 2 * NB + 4;     // halo: [NW] window slot loaded (TMA -> MMA)
+    uint64_t* empty_w = full_w + (HALO ? STAGES : 0);  // halo: [NW] window slot released (MMA -> TMA)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty_w + (HALO ? STAGES : 0));
+    float* epi_smem = reinterpret_cast<float*>(ring + ring_bytes);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? tc::cluster_ctarank() : 0u;
@@ -239,9 +273,15 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     const int group = blockIdx.x / CG, ngroups = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NB; ++s) {
             tc::mbar_init(tc::smem_u32(&full[s]), CG);  // leader: own arrive.expect_tx (+ the peer's arrive)
             tc::mbar_init(tc::smem_u32(&empty[s]), 1);
+        }
+        if constexpr (HALO) {
+            for (int s = 0; s < STAGES; ++s) {
+                tc::mbar_init(tc::smem_u32(&full_w[s]), CG);
+                tc::mbar_init(tc::smem_u32(&empty_w[s]), 1);
+            }
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(tc::smem_u32(&acc_full[a]), 1);
@@ -263,36 +303,118 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
 
     // this CTA's 128-row sub-tile of the group's tile
     auto sub_tile = [&](const Seg& w) { return w.mt * CG + (int)rank; };
+    // conv: (image, first output row, first output column) of this CTA's 128-pixel sub-tile;
+    // image >= N marks a padding sub-tile (TMA zero-fills its loads, its stores are clipped).
+    // Halo tiles run down the output rows (p fastest, then the column tile, then the image) so a
+    // CTA's consecutive tiles share R-1 input rows; a CTA pair splits the rows into two halves.
+    struct Px {
+        int img, p0, q0;
+    };
+    auto px_of = [&](const Seg& w) {
+        Px x;
+        if constexpr (HALO) {
+            const int ph = (p.P + CG - 1) / CG;
+            const int t = w.mt / ph;
+            x.p0 = w.mt % ph + (int)rank * ph;
+            x.q0 = (t % p.tiles_q) * 128;
+            x.img = t / p.tiles_q;
+            if (x.p0 >= p.P) x.img = p.N_img;  // the pair's second half ran past the last row
+        } else {
+            const int mt = sub_tile(w);
+            x.q0 = (mt % p.tiles_q) * TQ;
+            const int t = mt / p.tiles_q;
+            x.p0 = (t % p.tiles_p) * TP;
+            x.img = t / p.tiles_p;
+        }
+        return x;
+    };
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer: one continuous ring across units
-            int it = 0;
+            int ps = 0;         // ring stage of the next k-block
+            uint32_t pph = 0;   // and its phase parity
+            int b_nt = -1, b_loads = 0, wseq = 0, r_img = -1, r_p0 = -2, r_q0 = -1, r_nt = -1;  // halo state
+            int pseg = 0;
             SegIter si(p, group, ngroups);
             Seg w;
             while (si.next(p, ngroups, w)) {
                 const int mt = sub_tile(w);
                 int img = w.bz, p0 = 0, q0 = 0;
                 if constexpr (CONV) {
-                    q0 = (mt % p.tiles_q) * TQ;
-                    const int t = mt / p.tiles_q;
-                    p0 = (t % p.tiles_p) * TP;
-                    img = t / p.tiles_p;  // >= N for a padding sub-tile: TMA zero-fills it
+                    const Px x = px_of(w);
+                    img = x.img;
+                    p0 = x.p0;
+                    q0 = x.q0;
                 }
                 const int nb = w.nt * BN + (int)rank * Cfg::BNC;
-                for (int i = 0; i < w.nkb; ++i, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+                if constexpr (HALO) {
+                    const int RS = p.R * p.S, NW = STAGES;
+                    // B resident: every (channel block, tap) slice of the n-tile, loaded when it changes
+                    if (w.nt != b_nt) {
+                        tc::mbar_wait(tc::smem_u32(&empty[0]), ((uint32_t)b_loads & 1u) ^ 1u);
+                        const uint32_t fb = tc::smem_u32(&full[0]);
+                        if (rank == 0) tc::mbar_expect_tx(fb, (uint32_t)(CG * p.CB * RS * Cfg::B_BYTES));
+                        else tc::mbar_arrive_remote(fb, 0);
+                        for (int cb = 0; cb < p.CB; ++cb)
+                            for (int tap = 0; tap < RS; ++tap) {
+                                const uint32_t sb = tc::smem_u32(ring + (cb * RS + tap) * Cfg::B_BYTES);
+                                const int fr = tap / p.S, fs = tap - fr * p.S;
+                                if constexpr (CG == 2) tc::tma_load_4d_cg2(sb, &tmB, fb, cb * 64, fs, fr, nb);
+                                else tc::tma_load_4d(sb, &tmB, fb, cb * 64, fs, fr, nb);
+                            }
+                        b_nt = w.nt;
+                        ++b_loads;
+                    }
+                    // input-row windows (one TMA box of 128 + S - 1 pixels per channel block, OOB =
+                    // padding): all R for the first tile of a run, then the one new row per tile
+                    const bool cont = img == r_img && q0 == r_q0 && p0 == r_p0 + 1 && w.nt == r_nt;
+                    const uint32_t wb = (uint32_t)(p.CB * (128 + p.S - 1) * 128);
+                    for (int r = cont ? p.R - 1 : 0; r < p.R; ++r, ++wseq) {
+                        const int slot = wseq % NW;
+                        tc::mbar_wait(tc::smem_u32(&empty_w[slot]), ((uint32_t)(wseq / NW) & 1u) ^ 1u);
+                        const uint32_t fa = tc::smem_u32(&full_w[slot]);
+                        if (rank == 0) tc::mbar_expect_tx(fa, CG * wb);
+                        else tc::mbar_arrive_remote(fa, 0);
+                        const uint32_t wa = tc::smem_u32(aring + slot * p.a_stage_bytes);
+                        for (int cb = 0; cb < p.CB; ++cb) {
+                            const uint32_t dst = wa + (uint32_t)(cb * p.win_bytes);
+                            if constexpr (CG == 2)
+                                tc::tma_load_4d_cg2(dst, &tmA, fa, cb * 64, q0 - p.pw, p0 - p.ph + r, img);
+                            else tc::tma_load_4d(dst, &tmA, fa, cb * 64, q0 - p.pw, p0 - p.ph + r, img);
+                        }
+                    }
+                    r_img = img;
+                    r_p0 = p0;
+                    r_q0 = q0;
+                    r_nt = w.nt;
+                    if (pseg == 2) TC_TRACE(14);  // producer: windows of segment 2 issued
+                    ++pseg;
+                    continue;
+                }
+                // (channel block, filter column, filter row) of the segment's first k-block, then
+                // carried: no integer division per k-block
+                int cb = 0, fs = 0, fr = 0;
+                if constexpr (CONV) {
+                    cb = w.kb0 % p.CB;
+                    const int rs = w.kb0 / p.CB;
+                    fs = rs % p.S;
+                    fr = rs / p.S;
+                }
+                for (int i = 0; i < w.nkb; ++i) {
+                    const int s = ps;
+                    const uint32_t ph = pph;
+                    if (++ps == STAGES) {
+                        ps = 0;
+                        pph ^= 1u;
+                    }
                     tc::mbar_wait(tc::smem_u32(&empty[s]), ph ^ 1u);
                     const uint32_t fb = tc::smem_u32(&full[s]);
                     if (rank == 0) tc::mbar_expect_tx(fb, CG * Cfg::STAGE_BYTES);
                     else tc::mbar_arrive_remote(fb, 0);
-                    const uint32_t sa = tc::smem_u32(base + s * Cfg::STAGE_BYTES);
+                    const uint32_t sa = tc::smem_u32(ring + s * Cfg::STAGE_BYTES);
                     const uint32_t sb = sa + Cfg::A_BYTES;
                     const int kb = w.kb0 + i;
                     if constexpr (CONV) {
-                        const int cb = kb % p.CB;
-                        const int rs = kb / p.CB;
-                        const int fs = rs % p.S, fr = rs / p.S;
                         const int wq = q0 * p.sw - p.pw + fs * p.dw;
                         const int hp = p0 * p.sh - p.ph + fr * p.dh;
 #pragma unroll
@@ -304,6 +426,13 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                             } else {
                                 tc::tma_load_4d(sa + a * BM * 128, &tmA, fb, c0, wq, hp, img);
                                 tc::tma_load_4d(sb + a * Cfg::BNC * 128, &tmB, fb, c0, fs, fr, nb);
+                            }
+                        }
+                        if (++cb == p.CB) {
+                            cb = 0;
+                            if (++fs == p.S) {
+                                fs = 0;
+                                ++fr;
                             }
                         }
                     } else {
@@ -323,9 +452,18 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {  // ---- MMA issuer (the leader CTA of a pair)
+        if (rank == 0) {  // ---- MMA issuer (the leader CTA of a pair): the whole warp, one elected lane issues
             constexpr uint32_t idesc = tc::idesc_bf16(BM * CG, BN);
-            int it = 0, j = 0;
+            int j = 0;
+            int ms = 0;        // ring stage of the next k-block (generic)
+            uint32_t mph = 0;  // and its phase parity
+            const uint32_t ring_u32 = tc::smem_u32(ring);
+            // halo state: the resident B's n-tile and load count; the window slot of input row 0 of
+            // the current tile (s0) and the slot / phase the next fresh window lands in
+            int b_nt = -1, b_loads = 0, s0 = 0, nslot = 0, prev_mt = -2, row = 0;
+            uint32_t nph = 0;
+            bool have_run = false;
+            const int ph_rows = (p.P + CG - 1) / CG;
             SegIter si(p, group, ngroups);
             Seg w;
             for (; si.next(p, ngroups, w); ++j) {
@@ -333,27 +471,109 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                 tc::mbar_wait(tc::smem_u32(&acc_empty[a]), ((uint32_t)(j >> 1) & 1u) ^ 1u);
                 tc::tc_fence_after();
                 const uint32_t acc = tmem + (uint32_t)(a * BN);
-                for (int i = 0; i < w.nkb; ++i, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+                if constexpr (HALO) {
+                    const int NW = STAGES;
+                    auto commit = [&](uint32_t bar) {
+                        if constexpr (CG == 2) tc::umma_commit_cg2_w(bar);
+                        else tc::umma_commit_w(bar);
+                    };
+                    if (w.nt != b_nt) {  // a new resident B: release the old one once its MMAs finish
+                        if (b_loads > 0) commit(tc::smem_u32(&empty[0]));
+                        tc::mbar_wait(tc::smem_u32(&full[0]), (uint32_t)b_loads & 1u);
+                        tc::tc_fence_after();
+                        b_nt = w.nt;
+                        ++b_loads;
+                        prev_mt = -2;  // windows do not carry across n-tiles
+                    }
+                    // the next output row of the same run shares R-1 input rows with this one
+                    const bool cont = w.mt == prev_mt + 1 && row + 1 < ph_rows;
+                    row = cont ? row + 1 : w.mt % ph_rows;
+                    prev_mt = w.mt;
+                    // release the windows this tile drops (their readers are all issued: the commit
+                    // arrives when they complete), then wait for the rows it adds
+                    int fresh;
+                    if (cont) {
+                        commit(tc::smem_u32(&empty_w[s0]));
+                        s0 = s0 + 1 == NW ? 0 : s0 + 1;
+                        fresh = p.R - 1;
+                    } else {
+                        if (have_run) {
+                            int sl = s0;
+                            for (int r = 0; r < p.R; ++r) {
+                                commit(tc::smem_u32(&empty_w[sl]));
+                                sl = sl + 1 == NW ? 0 : sl + 1;
+                            }
+                        }
+                        s0 = nslot;
+                        fresh = 0;
+                        have_run = true;
+                    }
+                    if (lane == 0 && (j == 1 || j == 2)) TC_TRACE(10 + j);  // MMA: accumulator free, before the window waits
+                    for (int r = fresh; r < p.R; ++r) {
+                        tc::mbar_wait(tc::smem_u32(&full_w[nslot]), nph);
+                        if (++nslot == NW) {
+                            nslot = 0;
+                            nph ^= 1u;
+                        }
+                    }
+                    tc::tc_fence_after();
+                    if (lane == 0 && j == 2) TC_TRACE(13);  // MMA: windows of segment 2 landed
+                    // tap (r, s) of channel block cb = rows s .. s+127 of window r: a whole-row shift of
+                    // the start address (the 128B swizzle is a function of the absolute address, so the
+                    // view stays consistent with the TMA-written layout; tools/umma_shift_probe.cu).
+                    // Descriptors advance by constants: B slices are stored in (cb, r, s) order.
+                    uint64_t db = tc::sdesc_sw128(ring_u32);
+                    const uint64_t da_ring = tc::sdesc_sw128(tc::smem_u32(aring));
+                    const uint32_t slot_step = (uint32_t)p.a_stage_bytes >> 4, win_step = (uint32_t)p.win_bytes >> 4;
+                    uint32_t accum = 0u;
+                    for (int cb = 0; cb < p.CB; ++cb) {
+                        int sl = s0;
+                        for (int fr = 0; fr < p.R; ++fr) {
+                            const uint64_t drow = da_ring + (uint64_t)(sl * slot_step + cb * win_step);
+                            sl = sl + 1 == NW ? 0 : sl + 1;
+                            for (int fs = 0; fs < p.S; ++fs) {
+                                const uint64_t da = drow + (uint64_t)(fs * 8);  // fs rows of 128 B
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) {
+                                    if constexpr (CG == 2) tc::umma_bf16_cg2_w(acc, da + 2 * k, db + 2 * k, idesc, accum);
+                                    else tc::umma_bf16_w(acc, da + 2 * k, db + 2 * k, idesc, accum);
+                                    accum = 1u;
+                                }
+                                db += (uint64_t)(Cfg::B_BYTES >> 4);
+                            }
+                        }
+                    }
+                    commit(tc::smem_u32(&acc_full[a]));
+                    if (lane == 0 && j == 2) TC_TRACE(15);  // MMA: segment 2 issued
+                    continue;
+                }
+                // the issue loop is one thread's dependent scalar code: ring index and phase are
+                // carried (no division by the runtime STAGES), descriptors are a per-stage base plus
+                // compile-time offsets (the 14-bit address field of a descriptor is addr >> 4)
+                for (int i = 0; i < w.nkb; ++i) {
+                    const int s = ms;
+                    const uint32_t ph = mph;
+                    if (++ms == STAGES) {
+                        ms = 0;
+                        mph ^= 1u;
+                    }
                     tc::mbar_wait(tc::smem_u32(&full[s]), ph);
                     tc::tc_fence_after();
-                    const uint32_t sa = tc::smem_u32(base + s * Cfg::STAGE_BYTES);
-                    const uint32_t sb = sa + Cfg::A_BYTES;
+                    const uint32_t sa = ring_u32 + (uint32_t)(s * Cfg::STAGE_BYTES);
+                    const uint64_t da0 = tc::sdesc_sw128(sa), db0 = tc::sdesc_sw128(sa + Cfg::A_BYTES);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
-                        const uint32_t atom = k / 4, inner = (k % 4) * 32;
-                        const uint64_t da = tc::sdesc_sw128(sa + atom * BM * 128 + inner);
-                        const uint64_t db = tc::sdesc_sw128(sb + atom * Cfg::BNC * 128 + inner);
-                        if constexpr (CG == 2) tc::umma_bf16_cg2(acc, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
-                        else tc::umma_bf16(acc, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                        const uint32_t offa = ((k / 4) * BM * 128 + (k % 4) * 32) >> 4;
+                        const uint32_t offb = ((k / 4) * Cfg::BNC * 128 + (k % 4) * 32) >> 4;
+                        if constexpr (CG == 2) tc::umma_bf16_cg2_w(acc, da0 + offa, db0 + offb, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                        else tc::umma_bf16_w(acc, da0 + offa, db0 + offb, idesc, (i > 0 || k > 0) ? 1u : 0u);
                     }
                     // frees the stage (in both CTAs of a pair) when these MMAs finish
-                    if constexpr (CG == 2) tc::umma_commit_cg2(tc::smem_u32(&empty[s]));
-                    else tc::umma_commit(tc::smem_u32(&empty[s]));
+                    if constexpr (CG == 2) tc::umma_commit_cg2_w(tc::smem_u32(&empty[s]));
+                    else tc::umma_commit_w(tc::smem_u32(&empty[s]));
                 }
-                if constexpr (CG == 2) tc::umma_commit_cg2(tc::smem_u32(&acc_full[a]));
-                else tc::umma_commit(tc::smem_u32(&acc_full[a]));
+                if constexpr (CG == 2) tc::umma_commit_cg2_w(tc::smem_u32(&acc_full[a]));
+                else tc::umma_commit_w(tc::smem_u32(&acc_full[a]));
             }
         }
     } else {  // ---- epilogue: TMEM -> registers -> global
@@ -371,13 +591,12 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             const int a = j & 1;
             bool row_ok = mt < p.m_tiles;
             long long orow;  // output row index (GEMM row or NPQ pixel)
+            Px px{0, 0, 0};
             if constexpr (CONV) {
-                const int q0 = (mt % p.tiles_q) * TQ;
-                const int t = mt / p.tiles_q;
-                const int pp = (t % p.tiles_p) * TP + trow / TQ, qq = q0 + trow % TQ;
-                const int img = t / p.tiles_p;
-                row_ok = row_ok && pp < p.P && qq < p.Q;
-                orow = ((long long)img * p.P + pp) * p.Q + qq;
+                px = px_of(w);
+                const int pp = px.p0 + trow / TQ, qq = px.q0 + trow % TQ;
+                row_ok = px.img < p.N_img && pp < p.P && qq < p.Q;
+                orow = ((long long)px.img * p.P + pp) * p.Q + qq;
             } else {
                 const int m = mt * BM + trow;
                 row_ok = row_ok && m < p.M;
@@ -388,10 +607,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             int bx1 = 0, bx2 = 0, bx3 = 0;
             if constexpr (CONV) {
                 constexpr int TQW = TQ < 32 ? TQ : 32;
-                bx1 = (mt % p.tiles_q) * TQ + ((q * 32) % TQ);
-                const int t = mt / p.tiles_q;
-                bx2 = (t % p.tiles_p) * TP + (q * 32) / TQ * (TQ / TQW);
-                bx3 = t / p.tiles_p;
+                bx1 = px.q0 + ((q * 32) % TQ);
+                bx2 = px.p0 + (q * 32) / TQ * (TQ / TQW);
+                bx3 = px.img;
             } else {
                 bx1 = mt * BM + q * 32;
                 bx2 = w.bz;
@@ -620,19 +838,35 @@ static bool encode_f32(CUtensorMap* m, void* ptr, int rank, const cuuint64_t* di
 // shape (it accounts for the ~240 registers per thread of these kernels), capped by TMEM
 // (512 columns per SM) and by the shared-memory bound; never more than one group per CG SMs
 // times that.
+// dynamic shared memory of a launch.  Halo (TQ = 128): STAGES window slots of a_stage bytes (one
+// input row, every channel block) + the resident B (b_res bytes) instead of the k-block ring.
 template <int BN, int BK, int TQ, int CG, int EW>
-static long long tc_resident_groups(int num_sms, int stages) {
+static size_t tc_smem_bytes(int stages, int a_stage, int b_res) {
     using Cfg = TcCfg<BN, BK, CG, EW>;
-    static std::atomic<long long> cache[64][Cfg::MAX_STAGES + 1];
+    if constexpr (TQ == 128)
+        return 1024 + (size_t)stages * a_stage + (size_t)b_res + (size_t)Cfg::EPI_BYTES + 256;
+    else return Cfg::smem(stages);
+}
+
+template <int BN, int BK, int TQ, int CG, int EW>
+static long long tc_resident_groups(int num_sms, int stages, int a_stage, int b_res) {
+    using Cfg = TcCfg<BN, BK, CG, EW>;
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, int>, long long> cache;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-    long long v = cache[dev & 63][stages].load(std::memory_order_relaxed);
-    if (v > 0) return v;
+    const auto key = std::make_tuple(dev, stages, a_stage, b_res);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto f = cache.find(key);
+        if (f != cache.end()) return f->second;
+    }
+    const size_t smem = tc_smem_bytes<BN, BK, TQ, CG, EW>(stages, a_stage, b_res);
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(CG);
     cfg.blockDim = dim3(Cfg::THREADS);
-    cfg.dynamicSmemBytes = Cfg::smem(stages);
+    cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
@@ -645,13 +879,14 @@ static long long tc_resident_groups(int num_sms, int stages) {
         cudaGetLastError();
         clusters = 0;
     }
-    int per_sm = (int)((228 * 1024) / (Cfg::smem(stages) + 1024));
+    int per_sm = (int)((228 * 1024) / (smem + 1024));
     const int tmem_per_sm = (int)(512 / Cfg::TMEM_COLS);
     per_sm = per_sm < tmem_per_sm ? per_sm : tmem_per_sm;
     per_sm = per_sm < 1 ? 1 : per_sm;
     long long g = (long long)(num_sms / CG) * per_sm;
     if (clusters > 0 && clusters < g) g = clusters;
-    cache[dev & 63][stages].store(g, std::memory_order_relaxed);
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = g;
     return g;
 }
 
@@ -685,10 +920,22 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     if constexpr (CONV) {
         constexpr int TP = 128 / TQ;
         // X: NHWC as {C, W, H, N}, traversal strides (1, sw, sh, 1); box {64, TQ*sw, TP*sh, 1}
+        // (halo, TQ = 128: one input-row window {64, 128 + S - 1, 1, 1}, stride 1)
         cuuint64_t xd[4] = {(cuuint64_t)s.c, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)s.n};
         cuuint64_t xs[3] = {(cuuint64_t)s.c * 2, (cuuint64_t)(s.w * s.c * 2), (cuuint64_t)(s.h * s.w * s.c * 2)};
         cuuint32_t xb[4] = {64, (cuuint32_t)(TQ * s.sw), (cuuint32_t)(TP * s.sh), 1};
         cuuint32_t xe[4] = {1, (cuuint32_t)s.sw, (cuuint32_t)s.sh, 1};
+        if constexpr (TQ == 128) {
+            if (s.sh != 1 || s.sw != 1 || s.dh != 1 || s.dw != 1 || s.c % 64 || 128 + s.s - 1 > 256)
+                return cudaErrorInvalidConfiguration;
+            xb[1] = (cuuint32_t)(128 + s.s - 1);
+            xb[2] = 1;
+            if (c.sched != 0 || c.split != 1 || c.raster != 0 || c.stages < s.r + 1) return cudaErrorInvalidConfiguration;
+            p.R = (int)s.r;
+            p.win_bytes = (int)(((128 + s.s - 1) * 128 + 1023) / 1024 * 1024);  // one channel block's window
+            p.a_stage_bytes = (int)(s.c / 64) * p.win_bytes;                       // a slot: one input row
+            p.contiguous = 1;
+        }
         // W: KRSC as {C, S, R, K}; box {64, 1, 1, BN / CG}
         cuuint64_t wd[4] = {(cuuint64_t)s.c, (cuuint64_t)s.s, (cuuint64_t)s.r, (cuuint64_t)s.k};
         cuuint64_t ws[3] = {(cuuint64_t)s.c * 2, (cuuint64_t)(s.s * s.c * 2), (cuuint64_t)(s.r * s.s * s.c * 2)};
@@ -701,8 +948,9 @@ cudaError_t tc_launch(const LaunchCtx& c) {
         p.sh = s.sh; p.sw = s.sw; p.ph = s.ph; p.pw = s.pw; p.dh = s.dh; p.dw = s.dw;
         p.tiles_q = (int)((s.q + TQ - 1) / TQ);
         p.tiles_p = (int)((s.p + TP - 1) / TP);
-        p.kblocks = (int)(s.r * s.s) * p.CB;
+        p.kblocks = TQ == 128 ? p.CB : (int)(s.r * s.s) * p.CB;  // halo: a k-block = a channel block, all taps
         p.m_tiles = (int)s.n * p.tiles_p * p.tiles_q;
+        p.N_img = (int)s.n;
         p.batch = 1;
     } else {
         if (!make_kmajor_map(&ta, c.x, s.batch, s.M, s.K, Cfg::BM) ||
@@ -734,6 +982,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
         if (!ok) return cudaErrorInvalidValue;
     }
     p.mp_tiles = (p.m_tiles + CG - 1) / CG;
+    if constexpr (TQ == 128) p.mp_tiles = (int)s.n * p.tiles_q * ((p.P + CG - 1) / CG);  // pairs split the rows
     const long long tiles = (long long)p.batch * p.mp_tiles * p.n_tiles;
     const long long units = tiles * c.split;
     if (units >= (1ll << 31)) return cudaErrorInvalidValue;
@@ -750,9 +999,11 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     // spins heads on their tails, so every group MUST be resident at once): the occupancy
     // calculator's active clusters (registers, shared memory, cluster shape) capped by TMEM
     const int stages = c.stages;
-    if (stages < 2 || stages > Cfg::MAX_STAGES || Cfg::smem(stages) > 227 * 1024) return cudaErrorInvalidConfiguration;
+    const int b_res = TQ == 128 ? p.CB * p.R * p.S * Cfg::B_BYTES : 0;
+    const size_t smem = tc_smem_bytes<BN, BK, TQ, CG, EW>(stages, p.a_stage_bytes, b_res);
+    if (stages < 2 || stages > Cfg::MAX_STAGES || smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     p.stages = stages;
-    const long long groups_max = tc_resident_groups<BN, BK, TQ, CG, EW>(c.num_sms, stages);
+    const long long groups_max = tc_resident_groups<BN, BK, TQ, CG, EW>(c.num_sms, stages, p.a_stage_bytes, b_res);
     if (groups_max < 1) return cudaErrorInvalidConfiguration;
     long long groups = groups_max;
     if (c.sched >= 1) {
@@ -778,7 +1029,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     std::memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)(groups * CG));
     cfg.blockDim = dim3(Cfg::THREADS);
-    cfg.dynamicSmemBytes = Cfg::smem(stages);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -809,7 +1060,7 @@ cudaError_t tc_launch(const LaunchCtx& c) {
                      tiles, p.dp_tiles, p.rem_tiles, p.rem_chunks);
         for (unsigned i = 0; i < cfg.gridDim.x; i += CG) {
             std::fprintf(stderr, "cta %3u:", i);
-            for (int k = 0; k < 11; ++k)
+            for (int k = 0; k < 16; ++k)
                 std::fprintf(stderr, " %7.2f", h[i * 16 + k] ? (h[i * 16 + k] - t0) * 1e-3 : -1.0);
             std::fprintf(stderr, "\n");
         }
@@ -841,6 +1092,10 @@ void register_tc_gemm() {
     TC_SHAPES(8, 1) TC_SHAPES(8, 2)     // conv, 16 x 8 pixel sub-tiles
     TC_SHAPES(16, 1) TC_SHAPES(16, 2)   // conv, 8 x 16
     TC_SHAPES(32, 1) TC_SHAPES(32, 2)   // conv, 4 x 32
+    // conv, halo row tiles of 128 pixels (BK = 64: one channel block of the R input-row windows)
+    tc_register<64, 64, 128, 1>(); tc_register<128, 64, 128, 1>(); tc_register<192, 64, 128, 1>();
+    tc_register<256, 64, 128, 1>(); tc_register<64, 64, 128, 2>(); tc_register<128, 64, 128, 2>();
+    tc_register<192, 64, 128, 2>(); tc_register<256, 64, 128, 2>();
 }
 
 }  // namespace db200

@@ -64,7 +64,11 @@ static std::vector<SketchDesc> build_catalogue() {
     const std::vector<const char*> tcc_names = {"BM",     "BN",    "BK",     "STAGES", "SPLIT_K",
                                                 "TILE_Q", "SCHED", "RASTER", "EPI",    "EW"};
     std::vector<std::vector<int32_t>> tcc_vals(tc_vals.begin(), tc_vals.end() - 4);
-    tcc_vals.push_back({8, 16, 32});
+    // TILE_Q = 128: halo row tiles (stride-1 convs): a tile is 128 output pixels of one row; the R
+    // input-row windows of 128 + S - 1 pixels it needs sit in a ring of STAGES row slots and filter
+    // tap (r, s) is the row-shifted view of window r.  A CTA runs down the output rows, so each
+    // tile loads ONE new input row (not R*S shifted copies) and the weights stay resident.
+    tcc_vals.push_back({8, 16, 32, 128});
     tcc_vals.push_back({0, 1, 2});
     tcc_vals.push_back({0, 1, 2, 3});
     tcc_vals.push_back({1, 2});
@@ -227,6 +231,20 @@ static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
     if (sh.op == TUNER_OP_CONV2D) {
         const int tq = v[5], tp = 128 / tq;
         if (sh.c % 8) return false;
+        if (tq == 128) {  // halo row tiles: stride 1, no dilation, whole 64-channel blocks, BK = 64
+            if (sh.sh != 1 || sh.sw != 1 || sh.dh != 1 || sh.dw != 1 || sh.c % 64 || bk != 64) return false;
+            if (128 + sh.s - 1 > 256) return false;  // a window is one TMA box (extent <= 256)
+            // runs down the output rows in order: one schedule, no split-K / stream-K / raster variants
+            if (v[6] != 0 || split != 1 || v[7] != 0) return false;
+            if (stages < sh.r + 1) return false;  // STAGES = window slots: R rows + >= 1 prefetched
+            if (bn > 256 || (bm != 128 && bm != 256)) return false;
+            const int cg = bm / 128;
+            const int64_t cb = sh.c / 64;
+            const int64_t win = ((128 + sh.s - 1) * 128 + 1023) / 1024 * 1024;
+            const int64_t bres = cb * sh.r * sh.s * (bn / cg) * 64 * 2;  // every tap's B slice, resident
+            const int64_t smem = 1024 + (int64_t)stages * cb * win + bres + kTcEpiBytes + 256;
+            return smem <= 227 * 1024 && (sh.k + bn - 1) / bn <= 65535;
+        }
         if (sh.sh > 8 || sh.sw > 8) return false;                  // TMA traversal stride <= 8
         if (tq * sh.sw > 256 || tp * sh.sh > 256) return false;    // TMA box extent <= 256
         if (bk > 64 && sh.c < bk) return false;                    // a fully zero channel block
@@ -325,4 +343,17 @@ extern "C" const char* tuner_knob_name(int32_t sketch, int32_t knob) {
     const SketchDesc* d = sketch_desc(sketch);
     if (!d || knob < 0 || knob >= (int32_t)d->knob_names.size()) return nullptr;
     return d->knob_names[knob];
+}
+
+extern "C" tuner_status tuner_sketch_valid(int32_t op, const tuner_shape* shape, int32_t sketch, const int32_t* values,
+                                           int32_t nvalues, int32_t* valid) {
+    if (!shape || !values || !valid) return fail(TUNER_EINVAL, "NULL argument");
+    const SketchDesc* d = sketch_desc(sketch);
+    if (!d) return fail(TUNER_ERANGE, "unknown sketch id");
+    if (nvalues != (int32_t)d->values.size()) return fail(TUNER_EDIM, "one value per knob of the sketch");
+    ShapeInfo sh;
+    std::string why;
+    if (!make_shape_info(op, *shape, sh, why)) return fail(TUNER_EINVAL, why.c_str());
+    *valid = sketch_valid(sketch, sh, values) ? 1 : 0;
+    return TUNER_OK;
 }

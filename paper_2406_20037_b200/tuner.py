@@ -56,6 +56,15 @@ def sketches(op: str, dtype: str = "f32") -> List[int]:
     return [ids[i] for i in range(min(n.value, 32))]
 
 
+def sketch_valid(op: str, shape: Dict, sketch: int, values: Sequence[int], dtype: str = "f32") -> bool:
+    """The sketch's static validity rule for a point given by knob values (no handle, no device)."""
+    vals = (C.c_int32 * max(1, len(values)))(*[int(v) for v in values])
+    ok = C.c_int32()
+    L.check(L.lib().tuner_sketch_valid(L.OP[op], C.byref(_shape(op, shape, dtype)), sketch, vals, len(values),
+                                       C.byref(ok)))
+    return bool(ok.value)
+
+
 def sketch_space(sketch: int) -> List[List[int]]:
     """The full compiled knob space of a sketch: one value list per knob."""
     nk = C.c_int32()

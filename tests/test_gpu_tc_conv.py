@@ -25,6 +25,11 @@ CASES = [
     (1, 14, 15, 128, 40, 1, 1, (2, 2), (0, 0), (1, 1)),
     (1, 12, 13, 24, 32, 3, 2, (1, 2), (2, 1), (2, 1)),
     (1, 9, 9, 192, 136, 3, 3, (1, 1), (1, 1), (1, 1)),
+    # halo row tiles (TILE_Q = 128): two pixel tiles per row with a ragged second one, 5x5 taps
+    # over two channel blocks, no padding with a ragged n tile
+    (1, 6, 150, 64, 72, 3, 3, (1, 1), (1, 1), (1, 1)),
+    (1, 7, 40, 128, 64, 5, 5, (1, 1), (2, 2), (1, 1)),
+    (2, 5, 20, 64, 200, 3, 3, (1, 1), (0, 0), (1, 1)),
 ]
 
 
@@ -94,3 +99,20 @@ def test_tc_conv_harness_vgg_like():
     rep = t.droplet(t.best().point, 60)
     fl = 2 * 2 * 56 * 56 * 128 * 128 * 9
     print("tc conv best", t.values(rep["best"]), rep["best_cost"], "ns", fl / rep["best_cost"] / 1e3, "TF")
+
+
+def test_tc_conv_halo_tiles_exercised_and_exact():
+    """The halo sketch (TILE_Q = 128: R input-row windows staged once per channel block, tap (r, s)
+    = window r shifted by s rows) on integer inputs: every sampled halo schedule bit-exact."""
+    case = (1, 5, 133, 64, 40, 3, 3, (1, 1), (1, 1), (1, 1))
+    shape, xd, wd, yo, _ = case_tensors(case, "int")
+    y = torch.empty(yo.shape, device=xd.device)
+    t = Tuner("conv2d", shape, dtype="bf16", spaces=[(SK, sketch_space(SK))], x=xd, w=wd, y=y)
+    tq = sketch_space(SK)[5].index(128)
+    pts = [p for p in points(t, per_instance=12, seed=3) if p[1][5] == tq]
+    assert len(pts) >= 8
+    for p in pts:
+        y.fill_(float("nan"))
+        t.run(p, xd, wd, y)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), yo.astype(np.float32)), t.values(p)
