@@ -11,6 +11,7 @@
 // (y, r, a as fp32) with 128-bit loads, grid-stride, warp-shuffle max, one
 // atomicMax per block on the float's bit pattern (non-negative floats order
 // like their bits).
+#include <cstdlib>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -175,6 +176,9 @@ cudaError_t launch_reference(const ShapeInfo& s, const void* x, const void* w, f
 // split-K zeroing: dependents may launch as soon as every CTA of this grid has started
 __global__ void zero_splitk(float4* __restrict__ y4, long long n4, float* __restrict__ tail, int ntail) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // launched programmatically after the previous kernel in the stream: its launch overlaps that
+    // kernel's tail, the stores wait for it (Y may still be read or written by it)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride)
         y4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -182,12 +186,25 @@ __global__ void zero_splitk(float4* __restrict__ y4, long long n4, float* __rest
 }
 
 cudaError_t zero_for_splitk(float* y, long long n, cudaStream_t st) {
+    // DB200_SPLITK_NOZERO=1: a timing experiment only (what the zeroing launch costs); the
+    // split-K results are then WRONG, so it is never set by the library, the tests or the bench
+    static const bool nozero = std::getenv("DB200_SPLITK_NOZERO") != nullptr;
+    if (nozero) return cudaSuccess;
     const long long n4 = n / 4;  // Y is a cudaMalloc'ed fp32 tensor: 16-byte aligned
     const int ntail = (int)(n - 4 * n4);
     long long blocks = (n4 + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    zero_splitk<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<float4*>(y), n4, y + 4 * n4, ntail);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    pdl_attr(attr[0]);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, zero_splitk, reinterpret_cast<float4*>(y), n4, y + 4 * n4, ntail);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

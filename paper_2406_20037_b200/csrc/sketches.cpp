@@ -50,6 +50,8 @@ static std::vector<SketchDesc> build_catalogue() {
     // (concurrent CTAs share the B panel), 1 = N fastest (they share the A panel).
     // EPI (runtime): how the epilogue writes the fp32 tile, both staged through 128B-swizzled shared
     // memory: 1 = TMA stores (cp.async.bulk.tensor), 2 = coalesced 128-byte st.global segments.
+    // (Unstaged 128-bit stores straight from the TMEM registers were measured 7-50 % slower on
+    // every layer tried, the smem-bound N = 64 halo tiles included, and are not in the lattice.)
     // EW (compiled): epilogue warps, 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each
     // draining every other 32-column chunk).
     const std::vector<const char*> tc_names = {"BM", "BN", "BK", "STAGES", "SPLIT_K", "SCHED", "RASTER", "EPI", "EW"};

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--window-us", type=float, default=200.0)
+    ap.add_argument("--no-verify", action="store_true", help="skip output verification (timing experiments)")
     ap.add_argument("points", nargs="+", help="sketch:v1,v2,...")
     a = ap.parse_args()
     import torch
@@ -52,13 +53,13 @@ def main():
         sks.add(sk)
     spaces = [(sk, sketch_space(sk)) for sk in sorted(sks)]
     # coarse pass to size the windows, then the timed pass
-    t0 = Tuner(L["op"], shape, dtype=a.dtype, spaces=spaces, x=xd, w=wd, y=y, seed=1, repeats=3)
+    t0 = Tuner(L["op"], shape, dtype=a.dtype, spaces=spaces, x=xd, w=wd, y=y, seed=1, repeats=3, verify=not a.no_verify)
     coarse = [r.cost_ns for r in t0.measure(pts)]
     t0.close()
     fast = min(c for c in coarse if c > 0 and math.isfinite(c))
     num = max(1, int(math.ceil(a.window_us * 1e3 / fast)))
     t = Tuner(L["op"], shape, dtype=a.dtype, spaces=spaces, x=xd, w=wd, y=y, seed=1, repeats=10,
-              number=min(num, 4000))
+              number=min(num, 4000), verify=not a.no_verify)
     for s, p, r in zip(a.points, pts, t.measure(pts)):
         tf = layer_flops(L) / r.cost_ns / 1e3 if r.cost_ns > 0 else 0
         print(f"{a.layer} {s:40s} {r.cost_ns:9.0f} ns {tf:7.2f} TF/s {r.status} err {r.max_err:.1e}", flush=True)
