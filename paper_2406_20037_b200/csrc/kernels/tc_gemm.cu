@@ -270,6 +270,10 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? tc::cluster_ctarank() : 0u;
     if (threadIdx.x == 0) TC_TRACE(0);
+    // programmatic dependent launch: the next kernel in the stream may be launched now (its CTAs
+    // become resident as this kernel's exit); this kernel's own TMA loads and stores wait for its
+    // predecessor (griddepcontrol.wait) -- only the prologue (barriers, TMEM, tensor maps) overlaps
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int group = blockIdx.x / CG, ngroups = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
@@ -331,6 +335,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer: one continuous ring across units
+            griddep_wait();  // X / W may be written by the preceding kernel
             int ps = 0;         // ring stage of the next k-block
             uint32_t pph = 0;   // and its phase parity
             int b_nt = -1, b_loads = 0, wseq = 0, r_img = -1, r_p0 = -2, r_q0 = -1, r_nt = -1;  // halo state
@@ -577,7 +582,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             }
         }
     } else {  // ---- epilogue: TMEM -> registers -> global
-        if (p.split > 1) griddep_wait();  // split-K: Y zeroed by the prerequisite grid (PDL)
+        griddep_wait();  // Y is written by the preceding kernel (split-K: zeroed by it)
         const int q = warp & 3;          // TMEM lane quadrant this warp may access (warp % 4)
         const int ew = warp - 2;         // epilogue warp index 0..EW-1
         const int half = ew >> 2;        // EW = 8: which of the quadrant's two warps (chunk parity)
@@ -1037,11 +1042,8 @@ cudaError_t tc_launch(const LaunchCtx& c) {
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (c.split > 1) {  // launch early: producer and MMA warps run while Y is zeroed
-        pdl_attr(attr[1]);
-        cfg.numAttrs = 2;
-    }
+    pdl_attr(attr[1]);  // launch early: the prologue overlaps the preceding kernel's tail
+    cfg.numAttrs = 2;
     static const bool tracing = std::getenv("DB200_TC_TRACE") != nullptr;
     static unsigned long long* trace_buf = nullptr;
     if (tracing && !trace_buf && cudaMalloc(&trace_buf, 4096 * 16 * sizeof(unsigned long long)) != cudaSuccess)
