@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--explore", default="evolve", choices=["evolve", "random"],
                     help="exploration phase of DPAnsor: Ansor-style evolution (default) or uniform sampling")
     ap.add_argument("--droplet-budget", type=int, default=100)
+    ap.add_argument("--evolve-pop", type=int, default=64, help="evolutionary exploration: population per generation")
+    ap.add_argument("--evolve-elite", type=int, default=16, help="evolutionary exploration: parents (best measured)")
     ap.add_argument("--droplet-sketch-factor", type=float, default=1.5,
                     help="Droplet also starts from the best point of every other sketch within this factor "
                          "of the overall best (R-D17); 1.0 = the paper's single start")
@@ -307,7 +309,9 @@ def main():
         # sketch rule (Ansor's rules are hardware-dependent): a bf16 conv is tuned
         # on the tcgen05 sketch when TMA can address it (C % 8 == 0), else on the SIMT one
         if dtype == "bf16" and L["op"] == "conv2d":
-            sks = [3 if L["C"] % 8 == 0 else 4] + ([10] if L["C"] <= 16 else [])  # + direct conv (stems)
+            sks = ([3 if L["C"] % 8 == 0 else 4] + ([10] if L["C"] <= 16 else [])  # + direct conv (stems)
+                   + ([11] if L["C"] % 64 == 0 and tuple(L.get("stride", (1, 1))) == (1, 1)
+                      and tuple(L.get("dil", (1, 1))) == (1, 1) else []))  # + halo row tiles
             return [(sk, sketch_space(sk)) for sk in sks]
         return None
 
@@ -324,7 +328,8 @@ def main():
         t0 = time.perf_counter()
         tu = Tuner(L["op"], shape_of(L), dtype=dt, spaces=sp, x=xd, w=wd, y=y, seed=seed, group=group,
                    stream=stream, early_cut=args.early_cut, policy=args.droplet_policy)
-        smp = tu.evolve(args.n_sample) if args.explore == "evolve" else tu.sample(args.n_sample)
+        smp = (tu.evolve(args.n_sample, pop=args.evolve_pop, elite=args.evolve_elite) if args.explore == "evolve"
+               else tu.sample(args.n_sample))
         if not smp:  # no compiled sketch covers this layer (e.g. bf16 TMA needs C % 8 == 0)
             tu.close()
             rec.update(skipped="no statically valid schedule", candidates=0, launches=0, collectives=0)
@@ -550,6 +555,7 @@ def main():
                    "l2": "flushed between steps (256 MB write); candidate timings hot-L2 (back-to-back launches)",
                    "early_cut": args.early_cut, "droplet_policy": args.droplet_policy,
                    "droplet_sketch_factor": args.droplet_sketch_factor,
+                   "evolve": {"pop": args.evolve_pop, "elite": args.evolve_elite},
                    "parallelism": f"candidates sharded x{world}"},
         "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu_baseline,
         "tuning_wall_s": {"dpansor": round(dp_wall, 3), "baseline_10k": round(bl_wall, 3),

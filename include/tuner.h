@@ -212,7 +212,8 @@ void tuner_opts_default(tuner_opts* o);
  *   9 simt_direct_conv_f32 / 10 ..._bf16        direct conv, C <= 16 stems
  *   2 tc_gemm_bf16 / 3 tc_igemm_conv_bf16       tcgen05 / TMEM / TMA (bf16 in, fp32 out)
  *   4 simt_igemm_conv_bf16                      SIMT implicit GEMM on bf16 inputs
- *   5 simt_dwconv_f32 / 6 simt_dwconv_bf16      depthwise conv */
+ *   5 simt_dwconv_f32 / 6 simt_dwconv_bf16      depthwise conv
+ *   11 tc_halo_conv_bf16                        tcgen05 conv, halo row tiles (stride 1, C % 64 == 0) */
 tuner_status tuner_sketches(int32_t op, int32_t dtype, int32_t* ids, int32_t cap, int32_t* n_out);
 tuner_status tuner_sketch_space(int32_t sketch, int32_t* nknobs, int32_t* card, int32_t* values);
 /* The static validity rule of a sketch ("sketch rules are hardware-dependent"; P:596-599

@@ -17,3 +17,4 @@ SK_SIMT_PIPE_GEMM_F32 = 7
 SK_SIMT_PIPE_CONV_F32 = 8
 SK_SIMT_DIRECT_CONV_F32 = 9
 SK_SIMT_DIRECT_CONV_BF16 = 10
+SK_TC_HALO_CONV_BF16 = 11

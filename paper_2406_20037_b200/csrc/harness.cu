@@ -182,6 +182,11 @@ static LaunchFn resolve(const Tuner* t, const Pt& p, RuntimeKnobs& rk) {
             rk.epi = v[8];
             rk.cluster = v[0] / 128;
             return registry_find(kernel_key(sk, v[0], v[1], v[2], v[9], v[5]));
+        case SK_TC_HALO_CONV_BF16:  // BM, BN, EW (compiled, BK 64, tile = 128 pixels of a row) | STAGES, EPI
+            rk.stages = v[2];
+            rk.epi = v[3];
+            rk.cluster = v[0] / 128;
+            return registry_find(kernel_key(SK_TC_IGEMM_CONV_BF16, v[0], v[1], 64, v[4], 128));
         case SK_SIMT_DIRECT_CONV_F32:  // KT, TP (compiled) | PX, BKC, EPI
         case SK_SIMT_DIRECT_CONV_BF16:
             rk.dims[0] = v[2];

@@ -19,7 +19,8 @@ enum SketchId : int32_t {
     SK_SIMT_PIPE_CONV_F32 = 8,
     SK_SIMT_DIRECT_CONV_F32 = 9,
     SK_SIMT_DIRECT_CONV_BF16 = 10,
-    SK_COUNT = 11
+    SK_TC_HALO_CONV_BF16 = 11,
+    SK_COUNT = 12
 };
 
 // depthwise sketch: shared-memory bytes of a CTA (filters [R*S][ctv] + input window

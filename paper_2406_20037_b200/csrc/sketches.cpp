@@ -66,17 +66,23 @@ static std::vector<SketchDesc> build_catalogue() {
     const std::vector<const char*> tcc_names = {"BM",     "BN",    "BK",     "STAGES", "SPLIT_K",
                                                 "TILE_Q", "SCHED", "RASTER", "EPI",    "EW"};
     std::vector<std::vector<int32_t>> tcc_vals(tc_vals.begin(), tc_vals.end() - 4);
-    // TILE_Q = 128: halo row tiles (stride-1 convs): a tile is 128 output pixels of one row; the R
-    // input-row windows of 128 + S - 1 pixels it needs sit in a ring of STAGES row slots and filter
-    // tap (r, s) is the row-shifted view of window r.  A CTA runs down the output rows, so each
-    // tile loads ONE new input row (not R*S shifted copies) and the weights stay resident.
-    tcc_vals.push_back({8, 16, 32, 128});
+    tcc_vals.push_back({8, 16, 32});
     tcc_vals.push_back({0, 1, 2});
     tcc_vals.push_back({0, 1, 2, 3});
     tcc_vals.push_back({1, 2});
     tcc_vals.push_back({4, 8});
     c.push_back({SK_TC_IGEMM_CONV_BF16, "tc_igemm_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tcc_names,
                  tcc_vals});
+    // halo row tiles (a sketch of its own: a different loop structure, not a TILE_Q value -- its
+    // points would be a sliver of sketch 3's space, rarely drawn and unreachable by coordinate
+    // descent from it): stride-1 convs, a tile is 128 output pixels of one row; the R input-row
+    // windows of 128 + S - 1 pixels it needs sit in a ring of STAGES row slots and filter tap
+    // (r, s) is the row-shifted UMMA view of window r.  A CTA runs down the output rows, so each
+    // tile loads ONE new input row (not R*S shifted copies) and the weights stay resident.
+    const std::vector<const char*> tch_names = {"BM", "BN", "STAGES", "EPI", "EW"};
+    const std::vector<std::vector<int32_t>> tch_vals = {{128, 256}, {64, 128, 192, 256}, {2, 3, 4, 5, 6, 7, 8},
+                                                        {1, 2},     {4, 8}};
+    c.push_back({SK_TC_HALO_CONV_BF16, "tc_halo_conv_bf16", 1 << TUNER_OP_CONV2D, TUNER_BF16, tch_names, tch_vals});
     // the SIMT implicit-GEMM sketch on bf16 inputs (widened to fp32 at staging, fp32
     // accumulate): a second bf16 conv sketch, and the only one for C % 8 != 0 (TMA needs
     // 16-byte strides); a restricted compile-time lattice
@@ -233,20 +239,6 @@ static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
     if (sh.op == TUNER_OP_CONV2D) {
         const int tq = v[5], tp = 128 / tq;
         if (sh.c % 8) return false;
-        if (tq == 128) {  // halo row tiles: stride 1, no dilation, whole 64-channel blocks, BK = 64
-            if (sh.sh != 1 || sh.sw != 1 || sh.dh != 1 || sh.dw != 1 || sh.c % 64 || bk != 64) return false;
-            if (128 + sh.s - 1 > 256) return false;  // a window is one TMA box (extent <= 256)
-            // runs down the output rows in order: one schedule, no split-K / stream-K / raster variants
-            if (v[6] != 0 || split != 1 || v[7] != 0) return false;
-            if (stages < sh.r + 1) return false;  // STAGES = window slots: R rows + >= 1 prefetched
-            if (bn > 256 || (bm != 128 && bm != 256)) return false;
-            const int cg = bm / 128;
-            const int64_t cb = sh.c / 64;
-            const int64_t win = ((128 + sh.s - 1) * 128 + 1023) / 1024 * 1024;
-            const int64_t bres = cb * sh.r * sh.s * (bn / cg) * 64 * 2;  // every tap's B slice, resident
-            const int64_t smem = 1024 + (int64_t)stages * cb * win + bres + kTcEpiBytes + 256;
-            return smem <= 227 * 1024 && (sh.k + bn - 1) / bn <= 65535;
-        }
         if (sh.sh > 8 || sh.sw > 8) return false;                  // TMA traversal stride <= 8
         if (tq * sh.sw > 256 || tp * sh.sh > 256) return false;    // TMA box extent <= 256
         if (bk > 64 && sh.c < bk) return false;                    // a fully zero channel block
@@ -263,6 +255,22 @@ static bool tc_valid(const ShapeInfo& sh, const int32_t* v) {
     if (split > ktiles) return false;
     if ((int64_t)split * sh.batch > 65535) return false;
     return true;
+}
+
+static bool halo_valid(const ShapeInfo& sh, const int32_t* v) {
+    const int bm = v[0], bn = v[1], stages = v[2];
+    if (sh.dtype != TUNER_BF16 || sh.op != TUNER_OP_CONV2D) return false;
+    // stride 1, no dilation, whole 64-channel blocks (TMA boxes of 128 B rows)
+    if (sh.sh != 1 || sh.sw != 1 || sh.dh != 1 || sh.dw != 1 || sh.c % 64 || sh.k % 4) return false;
+    if (128 + sh.s - 1 > 256) return false;  // a window is one TMA box (extent <= 256)
+    if (stages < sh.r + 1) return false;     // STAGES = window slots: R rows + >= 1 prefetched
+    if (bn > 256 || (bm != 128 && bm != 256)) return false;
+    const int cg = bm / 128;
+    const int64_t cb = sh.c / 64;
+    const int64_t win = ((128 + sh.s - 1) * 128 + 1023) / 1024 * 1024;
+    const int64_t bres = cb * sh.r * sh.s * (bn / cg) * 64 * 2;  // every tap's B slice, resident
+    const int64_t smem = 1024 + (int64_t)stages * cb * win + bres + kTcEpiBytes + 256;
+    return smem <= 227 * 1024 && (sh.k + bn - 1) / bn <= 65535;
 }
 
 static bool dw_valid(const ShapeInfo& sh, const int32_t* v) {
@@ -301,6 +309,7 @@ bool sketch_valid(int32_t id, const ShapeInfo& sh, const int32_t* v) {
         case SK_TC_IGEMM_CONV_BF16: return tc_valid(sh, v);
         case SK_SIMT_DWCONV_F32:
         case SK_SIMT_DWCONV_BF16: return dw_valid(sh, v);
+        case SK_TC_HALO_CONV_BF16: return halo_valid(sh, v);
         default: return false;
     }
 }

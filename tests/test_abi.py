@@ -43,7 +43,7 @@ def test_catalogue():
     assert sketches("dense", "f32") == [0, 7]
     assert sketches("batch_matmul", "f32") == [0, 7]
     assert sketches("conv2d", "f32") == [1, 8, 9]
-    assert sketches("conv2d", "bf16") == [3, 4, 10]
+    assert sketches("conv2d", "bf16") == [3, 11, 4, 10]
     assert sketches("dense", "bf16") == [2]
     assert sketch_name(0) == "simt_gemm_f32"
     assert knob_names(0) == ["BM", "BN", "BK", "TT", "UNROLL", "VEC", "STAGES", "SPLIT_K"]
@@ -55,6 +55,8 @@ def test_catalogue():
     assert knob_names(8) == ["BM", "BN", "BK", "TT", "KW", "VEC", "STAGES", "SPLIT_K", "OCC", "RED"]
     assert sketch_name(10) == "simt_direct_conv_bf16"
     assert knob_names(9) == ["KT", "TP", "PX", "BKC", "EPI"]
+    assert sketch_name(11) == "tc_halo_conv_bf16"
+    assert knob_names(11) == ["BM", "BN", "STAGES", "EPI", "EW"]
     assert sketch_name(99) is None
 
 

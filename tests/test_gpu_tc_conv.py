@@ -101,15 +101,47 @@ def test_tc_conv_harness_vgg_like():
     print("tc conv best", t.values(rep["best"]), rep["best_cost"], "ns", fl / rep["best_cost"] / 1e3, "TF")
 
 
-def test_tc_conv_halo_tiles_exercised_and_exact():
-    """The halo sketch (TILE_Q = 128: R input-row windows staged once per channel block, tap (r, s)
-    = window r shifted by s rows) on integer inputs: every sampled halo schedule bit-exact."""
+HALO_CASES = [
+    # N, H, W, C, K, R, S, stride, pad, dil -- stride 1, C % 64 == 0
+    (2, 20, 18, 64, 64, 3, 3, (1, 1), (1, 1), (1, 1)),
+    (1, 6, 150, 64, 72, 3, 3, (1, 1), (1, 1), (1, 1)),     # two pixel tiles per row, the second ragged
+    (2, 5, 20, 64, 200, 3, 3, (1, 1), (0, 0), (1, 1)),     # no padding, ragged n tile
+    (1, 7, 40, 64, 64, 2, 2, (1, 1), (0, 1), (1, 1)),      # 2 x 2 taps, asymmetric padding
+    (1, 9, 30, 128, 48, 1, 1, (1, 1), (0, 0), (1, 1)),     # 1 x 1, two channel blocks per row slot
+]
+
+
+@pytest.mark.parametrize("case", HALO_CASES)
+def test_tc_halo_all_configs_vs_oracle(case):
+    """Sketch 11 (halo row tiles: R input-row windows staged once per row, tap (r, s) = window r
+    shifted by s rows, resident weights): every valid point vs the oracle."""
+    shape, xd, wd, yo, ao = case_tensors(case, "uniform")
+    y = torch.empty(yo.shape, device=xd.device)
+    t = Tuner("conv2d", shape, dtype="bf16", spaces=[(11, sketch_space(11))], x=xd, w=wd, y=y)
+    vals = sketch_space(11)
+    pts = [(11, idx) for idx in itertools.product(*[range(len(v)) for v in vals]) if t.valid((11, idx))]
+    assert pts
+    bad, worst = [], 0.0
+    for p in pts:
+        y.fill_(float("nan"))
+        t.run(p, xd, wd, y)
+        torch.cuda.synchronize()
+        e = on.max_rel_err(y.cpu().numpy(), yo, ao)
+        worst = max(worst, e)
+        if not e <= 1e-5:
+            bad.append((t.values(p), e))
+    assert not bad, bad[:5]
+    print(case, len(pts), "halo configs, worst err", worst)
+
+
+def test_tc_halo_exact_integer_inputs():
+    """Integer inputs: every halo schedule bit-exact (pixel tiles ragged in both directions)."""
     case = (1, 5, 133, 64, 40, 3, 3, (1, 1), (1, 1), (1, 1))
     shape, xd, wd, yo, _ = case_tensors(case, "int")
     y = torch.empty(yo.shape, device=xd.device)
-    t = Tuner("conv2d", shape, dtype="bf16", spaces=[(SK, sketch_space(SK))], x=xd, w=wd, y=y)
-    tq = sketch_space(SK)[5].index(128)
-    pts = [p for p in points(t, per_instance=12, seed=3) if p[1][5] == tq]
+    t = Tuner("conv2d", shape, dtype="bf16", spaces=[(11, sketch_space(11))], x=xd, w=wd, y=y)
+    vals = sketch_space(11)
+    pts = [(11, idx) for idx in itertools.product(*[range(len(v)) for v in vals]) if t.valid((11, idx))]
     assert len(pts) >= 8
     for p in pts:
         y.fill_(float("nan"))

@@ -82,7 +82,9 @@ def main():
             y = torch.empty(yshape, device=dev)
             spaces = None
             if a.dtype == "bf16" and L["op"] == "conv2d":
-                sks = [3 if L["C"] % 8 == 0 else 4] + ([10] if L["C"] <= 16 else [])  # + direct conv (stems)
+                sks = ([3 if L["C"] % 8 == 0 else 4] + ([10] if L["C"] <= 16 else [])  # + direct conv (stems)
+                   + ([11] if L["C"] % 64 == 0 and tuple(L.get("stride", (1, 1))) == (1, 1)
+                      and tuple(L.get("dil", (1, 1))) == (1, 1) else []))  # + halo row tiles
                 spaces = [(sk, sketch_space(sk)) for sk in sks]
             fl = layer_flops(L)
             rec = {"model": mname, "layer": L["name"], "op": L["op"], "count": L["count"], "gflop": fl / 1e9,
