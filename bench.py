@@ -136,7 +136,8 @@ def traffic_evidence(tuned):
     best schedules, from the committed ncu --set full captures (profiles/traffic_r2.json, written by
     tools/capture_traffic.py from a bench run's best schedules; ncu flushes the caches before each
     replay, so these are cold-cache bytes).  Mean over the timed layers that have a capture."""
-    path = os.path.join(ROOT, "profiles", "traffic_r2.json")
+    name = "traffic_r2b.json" if os.path.exists(os.path.join(ROOT, "profiles", "traffic_r2b.json")) else "traffic_r2.json"
+    path = os.path.join(ROOT, "profiles", name)
     try:
         cap = json.load(open(path))
     except Exception:
@@ -146,7 +147,7 @@ def traffic_evidence(tuned):
         return None
     same = sum(1 for r in tuned if r["layer"] in cap and cap[r["layer"]].get("schedule") == r.get("dp_best"))
     return {"dram_bytes_per_launch": sum(g["dram_bytes"] for g in got) / len(got),
-            "source": f"profiles/traffic_r2.json: {len(got)}/{len(tuned)} timed layers captured "
+            "source": f"profiles/{name}: {len(got)}/{len(tuned)} timed layers captured "
                       f"({same} with this run's exact best schedule)"}
 
 
