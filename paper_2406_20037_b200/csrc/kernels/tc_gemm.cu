@@ -338,7 +338,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             griddep_wait();  // X / W may be written by the preceding kernel
             int ps = 0;         // ring stage of the next k-block
             uint32_t pph = 0;   // and its phase parity
-            int b_nt = -1, b_loads = 0, wseq = 0, r_img = -1, r_p0 = -2, r_q0 = -1, r_nt = -1;  // halo state
+            int b_nt = -1, b_loads = 0, wseq = 0, r_mt = -2, r_row = 0, r_nt = -1;  // halo state
+            const int ph_rows_p = (p.P + CG - 1) / CG;
             int pseg = 0;
             SegIter si(p, group, ngroups);
             Seg w;
@@ -371,8 +372,12 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                         ++b_loads;
                     }
                     // input-row windows (one TMA box of 128 + S - 1 pixels per channel block, OOB =
-                    // padding): all R for the first tile of a run, then the one new row per tile
-                    const bool cont = img == r_img && q0 == r_q0 && p0 == r_p0 + 1 && w.nt == r_nt;
+                    // padding): all R for the first tile of a run, then the one new row per tile.  The
+                    // run rule is the MMA issuer's, on the group's tile index (both CTAs of a pair and
+                    // the issuer must agree; a pair's padding row past P continues its run)
+                    const bool cont = w.mt == r_mt + 1 && r_row + 1 < ph_rows_p && w.nt == r_nt;
+                    r_row = cont ? r_row + 1 : w.mt % ph_rows_p;
+                    r_mt = w.mt;
                     const uint32_t wb = (uint32_t)(p.CB * (128 + p.S - 1) * 128);
                     for (int r = cont ? p.R - 1 : 0; r < p.R; ++r, ++wseq) {
                         const int slot = wseq % NW;
@@ -388,9 +393,6 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
                             else tc::tma_load_4d(dst, &tmA, fa, cb * 64, q0 - p.pw, p0 - p.ph + r, img);
                         }
                     }
-                    r_img = img;
-                    r_p0 = p0;
-                    r_q0 = q0;
                     r_nt = w.nt;
                     if (pseg == 2) TC_TRACE(14);  // producer: windows of segment 2 issued
                     ++pseg;

@@ -108,6 +108,9 @@ HALO_CASES = [
     (2, 5, 20, 64, 200, 3, 3, (1, 1), (0, 0), (1, 1)),     # no padding, ragged n tile
     (1, 7, 40, 64, 64, 2, 2, (1, 1), (0, 1), (1, 1)),      # 2 x 2 taps, asymmetric padding
     (1, 9, 30, 128, 48, 1, 1, (1, 1), (0, 0), (1, 1)),     # 1 x 1, two channel blocks per row slot
+    # more tiles than CTAs (pairs): runs of several rows per CTA, P odd (a pair's last row is padding
+    # in mid-run), runs crossing images
+    (16, 33, 20, 64, 64, 3, 3, (1, 1), (1, 1), (1, 1)),
 ]
 
 
