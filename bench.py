@@ -306,13 +306,22 @@ def main():
 
     from paper_2406_20037_b200 import sketch_space
 
+    def halo_fits(L):
+        """Sketch 11 (halo row tiles) has a statically valid point for this layer (stride 1, C % 64 == 0
+        and its rows + resident weights fit shared memory: C = 64 layers in practice)."""
+        import itertools
+        from paper_2406_20037_b200 import sketch_valid
+        if L["C"] % 64 or tuple(L.get("stride", (1, 1))) != (1, 1):
+            return False
+        shp = {k: L[k] for k in ("N", "C", "H", "W", "K", "R", "S", "stride", "pad", "dil") if k in L}
+        return any(sketch_valid("conv2d", shp, 11, list(v), "bf16") for v in itertools.product(*sketch_space(11)))
+
     def spaces_of(L):
         # sketch rule (Ansor's rules are hardware-dependent, P:166): a bf16 conv is tuned
         # on the tcgen05 sketch when TMA can address it (C % 8 == 0), else on the SIMT one
         if dtype == "bf16" and L["op"] == "conv2d":
             sks = ([3 if L["C"] % 8 == 0 else 4] + ([10] if L["C"] <= 16 else [])  # + direct conv (stems)
-                   + ([11] if L["C"] % 64 == 0 and tuple(L.get("stride", (1, 1))) == (1, 1)
-                      and tuple(L.get("dil", (1, 1))) == (1, 1) else []))  # + halo row tiles
+                   + ([11] if halo_fits(L) else []))  # + halo row tiles where the sketch has valid points
             return [(sk, sketch_space(sk)) for sk in sks]
         return None
 

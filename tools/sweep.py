@@ -38,9 +38,16 @@ def main():
     a = ap.parse_args()
     import torch
 
-    from paper_2406_20037_b200 import Tuner, sketch_space
+    from paper_2406_20037_b200 import Tuner, sketch_space, sketch_valid
     from synth import MODELS, layer_flops, layer_tensors, model_layers
     from synth.workloads import out_hw
+
+    def halo_fits(L):  # sketch 11 has a statically valid point for this layer (as in bench.py)
+        import itertools
+        if L["C"] % 64 or tuple(L.get("stride", (1, 1))) != (1, 1):
+            return False
+        shp = {k: L[k] for k in ("N", "C", "H", "W", "K", "R", "S", "stride", "pad", "dil") if k in L}
+        return any(sketch_valid("conv2d", shp, 11, list(v), "bf16") for v in itertools.product(*sketch_space(11)))
 
     mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -83,8 +90,7 @@ def main():
             spaces = None
             if a.dtype == "bf16" and L["op"] == "conv2d":
                 sks = ([3 if L["C"] % 8 == 0 else 4] + ([10] if L["C"] <= 16 else [])  # + direct conv (stems)
-                   + ([11] if L["C"] % 64 == 0 and tuple(L.get("stride", (1, 1))) == (1, 1)
-                      and tuple(L.get("dil", (1, 1))) == (1, 1) else []))  # + halo row tiles
+                       + ([11] if halo_fits(L) else []))  # + halo row tiles where the sketch has valid points
                 spaces = [(sk, sketch_space(sk)) for sk in sks]
             fl = layer_flops(L)
             rec = {"model": mname, "layer": L["name"], "op": L["op"], "count": L["count"], "gflop": fl / 1e9,
