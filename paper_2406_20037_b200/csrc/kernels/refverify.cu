@@ -175,10 +175,10 @@ cudaError_t launch_reference(const ShapeInfo& s, const void* x, const void* w, f
 
 // split-K zeroing: dependents may launch as soon as every CTA of this grid has started
 __global__ void zero_splitk(float4* __restrict__ y4, long long n4, float* __restrict__ tail, int ntail) {
+    // launched with plain stream serialisation: it starts after the previous kernel completed, so
+    // the partial-sum kernel launched programmatically behind it may read X at once (its
+    // predecessor's predecessor is complete) and waits for this one only before its first atomic
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    // launched programmatically after the previous kernel in the stream: its launch overlaps that
-    // kernel's tail, the stores wait for it (Y may still be read or written by it)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride)
         y4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -195,16 +195,7 @@ cudaError_t zero_for_splitk(float* y, long long n, cudaStream_t st) {
     long long blocks = (n4 + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)blocks);
-    cfg.blockDim = dim3(256);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    pdl_attr(attr[0]);
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, zero_splitk, reinterpret_cast<float4*>(y), n4, y + 4 * n4, ntail);
-    if (e != cudaSuccess) return e;
+    zero_splitk<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<float4*>(y), n4, y + 4 * n4, ntail);
     return cudaGetLastError();
 }
 

@@ -313,10 +313,10 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
     };
 
     // launched with programmatic stream serialization: the prologue above overlaps the preceding
-    // kernel's tail; X and W are read only after it completed (split-K: the preceding kernel is this
-    // schedule's zeroing launch, itself programmatic behind the kernel before it, so the wait also
-    // covers Y being zeroed)
-    griddep_wait();
+    // kernel's tail; X and W are read only after it completed -- except behind this schedule's own
+    // split-K zeroing kernel, which is plainly serialised (every earlier kernel is complete when it
+    // starts), so the wait is deferred to the first atomic (Y zeroed)
+    if (p.split == 1) griddep_wait();
     if (p.stages >= 2) {  // STAGES = 2: register prefetch of the next tile overlaps the FMAs
         gload(kt_begin);
         sstore(0);
@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(SimtCfg<BM, BN, BK, TT>::NT)
 
     // epilogue: direct stores (SPLIT_K = 1) or atomic partial-sum reduction
     const bool atomic = p.split > 1;
+    if (atomic) griddep_wait();  // Y zeroed by the prerequisite grid (PDL)
 #pragma unroll
     for (int i = 0; i < TT; ++i) {
         const int m = m0 + tile_row<BM, TT>(ty, i);

@@ -351,6 +351,7 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
     auto epilogue = [&](const Unit& w) {
         if (p.cred) return epilogue_cluster(w);
         float* __restrict__ C = p.C + w.bz * p.sC;
+        if (atomic) griddep_wait();  // Y zeroed by the prerequisite grid (PDL); returns at once later
         if (!staged_epi) {  // KW = 1, no split-K: direct stores from the accumulators
 #pragma unroll
             for (int i = 0; i < TT; ++i) {
@@ -419,10 +420,10 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT) * KW) simt_pipe_kernel(c
         }
     };
     // Launched with programmatic stream serialization: the prologue above (k table, slot setup)
-    // overlaps the preceding kernel's tail; X and W are read only after that kernel completed
-    // (split-K: the preceding kernel is this schedule's zeroing launch, itself programmatic behind
-    // the kernel before it, so the wait also covers Y being zeroed).
-    griddep_wait();
+    // overlaps the preceding kernel's tail.  X and W are read only after that kernel completed --
+    // except behind this schedule's own split-K zeroing kernel (plainly serialised, so every
+    // earlier kernel is complete when it starts), where the wait is deferred to the first atomic.
+    if (!atomic) griddep_wait();
     for (int s = 0; s < stages - 1; ++s) {
         produce(s);
         cp_commit();

@@ -335,7 +335,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer: one continuous ring across units
-            griddep_wait();  // X / W may be written by the preceding kernel
+            // X / W may be written by the preceding kernel; behind a split-K zeroing kernel (plainly
+            // serialised) every earlier kernel is already complete
+            if (p.split == 1) griddep_wait();
             int ps = 0;         // ring stage of the next k-block
             uint32_t pph = 0;   // and its phase parity
             int b_nt = -1, b_loads = 0, wseq = 0, r_mt = -2, r_row = 0, r_nt = -1;  // halo state
