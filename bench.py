@@ -52,6 +52,8 @@ def parse():
                     help="Droplet step rule: plain (the paper's text), grow (R-D9), radius (R-D16)")
     ap.add_argument("--baseline", type=int, default=10000)
     ap.add_argument("--early-cut", type=float, default=4.0)
+    ap.add_argument("--candidate-warmup", type=int, default=2,
+                    help="untimed windows per candidate before its timed repeats (after its verify run)")
     ap.add_argument("--repeats", type=int, default=3,
                     help="timed windows per candidate: 3, the paper's 'averages of three samples' (P:410, R-M2); "
                          "near-best candidates are re-timed over long windows by the precise tier (R-M4)")
@@ -340,7 +342,8 @@ def main():
         # DPAnsor: explore N, best-of-N, Droplet to convergence (<= 100 trials)
         t0 = time.perf_counter()
         tu = Tuner(L["op"], shape_of(L), dtype=dt, spaces=sp, x=xd, w=wd, y=y, seed=seed, group=group,
-                   stream=stream, early_cut=args.early_cut, policy=args.droplet_policy, repeats=args.repeats)
+                   stream=stream, early_cut=args.early_cut, policy=args.droplet_policy, repeats=args.repeats,
+                   warmup=args.candidate_warmup)
         smp = (tu.evolve(args.n_sample, pop=args.evolve_pop, elite=args.evolve_elite) if args.explore == "evolve"
                else tu.sample(args.n_sample))
         if not smp:  # no compiled sketch covers this layer (e.g. bf16 TMA needs C % 8 == 0)
@@ -369,7 +372,8 @@ def main():
         cut, precise = st["early_cut"], st["precise"]
         # the 10,000-trial random baseline on the same harness (fresh history, other seed)
         bl = Tuner(L["op"], shape_of(L), dtype=dt, spaces=sp, x=xd, w=wd, y=y, seed=seed + 7919,
-                   group=group, stream=stream, early_cut=args.early_cut, repeats=args.repeats)
+                   group=group, stream=stream, early_cut=args.early_cut, repeats=args.repeats,
+                   warmup=args.candidate_warmup)
         bl.sample(args.baseline) if args.baseline > 0 else None
         t2 = time.perf_counter()
         bst = bl.stats()
@@ -566,7 +570,7 @@ def main():
         "config": {"workload": f"{args.workload} layers ({dtype}): {args.n_sample} samples + Droplet "
                                f"(<= {args.droplet_budget}) vs {args.baseline}-trial random baseline, one layer per step",
                    "l2": "flushed between steps (256 MB write); candidate timings hot-L2 (back-to-back launches)",
-                   "early_cut": args.early_cut, "repeats": args.repeats, "droplet_policy": args.droplet_policy,
+                   "early_cut": args.early_cut, "repeats": args.repeats, "candidate_warmup": args.candidate_warmup, "droplet_policy": args.droplet_policy,
                    "droplet_sketch_factor": args.droplet_sketch_factor,
                    "evolve": {"pop": args.evolve_pop, "elite": args.evolve_elite},
                    "parallelism": f"candidates sharded x{world}"},
