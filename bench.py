@@ -51,7 +51,9 @@ def parse():
     ap.add_argument("--droplet-policy", default="grow", choices=["plain", "grow", "radius"],
                     help="Droplet step rule: plain (the paper's text), grow (R-D9), radius (R-D16)")
     ap.add_argument("--baseline", type=int, default=10000)
-    ap.add_argument("--early-cut", type=float, default=4.0)
+    ap.add_argument("--early-cut", type=float, default=2.0,
+                    help="R-M3: a candidate whose verify run exceeds this factor x the best verify run known is "
+                         "ranked by that run (executed and verified, one timed launch); the fraction is reported")
     ap.add_argument("--candidate-warmup", type=int, default=2,
                     help="untimed windows per candidate before its timed repeats (after its verify run)")
     ap.add_argument("--repeats", type=int, default=3,

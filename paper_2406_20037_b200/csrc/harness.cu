@@ -25,6 +25,8 @@
 #include <chrono>
 #include <cstdint>
 #include <thread>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_set>
@@ -279,7 +281,16 @@ struct GpuMeasurer : Measurer {
     // precise one (R-M4), which is systematically below both, so it is not compared with them.
     double best_tver = INFINITY, best_coarse = INFINITY;
 
+    // DB200_HOST_PROF=1: host seconds per phase (verify incl. its wait, time, precise; wait of verify)
+    double hprof[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    size_t hprof_n = 0;
     ~GpuMeasurer() override {
+        if (std::getenv("DB200_HOST_PROF") && hprof_n)
+            std::fprintf(stderr, "HOST_PROF candidates %zu: verify %.3f s (waiting %.3f), time %.3f s (waiting %.3f), precise %.3f s -> %.1f us/cand\n",
+                         hprof_n, hprof[0], hprof[3], hprof[1], hprof[4], hprof[2], 1e6 * (hprof[0] + hprof[1] + hprof[2]) / hprof_n);
+        if (std::getenv("DB200_HOST_PROF") && hprof_n)
+            std::fprintf(stderr, "HOST_PROF detail: first-launch %.3f s, verify launch+memset+events %.3f s, capture %.3f s, exec update %.3f s\n",
+                         hprof[5], hprof[6], hprof[7], hprof[8]);
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(dev);
@@ -361,11 +372,14 @@ struct GpuMeasurer : Measurer {
         LaunchCtx cc = b.ctx;
         cc.stream = cap;
         set_capturing(true);
+        const auto q0 = std::chrono::steady_clock::now();
         cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
         for (int i = 0; i < G && e == cudaSuccess; ++i) e = b.fn[j](cc);
         cudaGraph_t g = nullptr;
         cudaError_t e2 = cudaStreamEndCapture(cap, &g);
         set_capturing(false);
+        const auto q1 = std::chrono::steady_clock::now();
+        hprof[7] += std::chrono::duration<double>(q1 - q0).count();
         if (e != cudaSuccess) return cuda_fail(e, "graph capture");
         if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamEndCapture");
         // family: sketch, cluster size, and whether a split-K zeroing node precedes each launch
@@ -374,6 +388,8 @@ struct GpuMeasurer : Measurer {
                              ((uint64_t)(b.rk[j].split > 1) << 15) | (uint64_t)(b.rk[j].cluster & 0x7FFF);
         e = exec_for(g, fam, b.execs[j]);
         cudaGraphDestroy(g);
+        const auto q2 = std::chrono::steady_clock::now();
+        hprof[8] += std::chrono::duration<double>(q2 - q1).count();
         if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
         CU(cudaEventRecord(ev[base], st));
         for (int r = 0; r < nwin; ++r) {
@@ -421,13 +437,18 @@ struct GpuMeasurer : Measurer {
             // one untimed launch the first time a launcher runs: module loading never
             // inflates t_verify (and so never causes a false early cut)
             cudaError_t e = b.fn[j] ? cudaSuccess : cudaErrorInvalidDeviceFunction;
+            const auto q0 = std::chrono::steady_clock::now();
             if (e == cudaSuccess && first_launch(dev, b.fn[j])) e = b.fn[j](b.ctx);
+            const auto q1 = std::chrono::steady_clock::now();
             if (e == cudaSuccess) {
                 if (t->opts.verify) CU(cudaMemsetAsync(t->opts.y, 0xFF, ybytes, st));
                 CU(cudaEventRecord(ev[2 * j], st));
                 e = b.fn[j](b.ctx);
                 CU(cudaEventRecord(ev[2 * j + 1], st));
             }
+            const auto q2 = std::chrono::steady_clock::now();
+            hprof[5] += std::chrono::duration<double>(q1 - q0).count();
+            hprof[6] += std::chrono::duration<double>(q2 - q1).count();
             if (e != cudaSuccess) {
                 cudaGetLastError();
                 out[j].status = TUNER_S_LAUNCH_FAIL;
@@ -439,8 +460,10 @@ struct GpuMeasurer : Measurer {
                 CU(launch_verify((const float*)t->opts.y, ref, absref, t->info.y_elems, d_err + j, nsm, st));
         }
         CU(cudaMemcpyAsync(h_err, d_err, n * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        const auto hw0 = std::chrono::steady_clock::now();
         if ((s = wait_progress(b.prog, b.stall_ms)) != TUNER_OK) return s;
         CU(cudaStreamSynchronize(st));
+        hprof[3] += std::chrono::duration<double>(std::chrono::steady_clock::now() - hw0).count();
         for (size_t j = 0; j < n; ++j) {
             if (!b.launched[j]) continue;
             float ms = 0.f;
@@ -466,7 +489,9 @@ struct GpuMeasurer : Measurer {
             set_knobs(b, j);
             int num = t->opts.number;
             if (num <= 0) {
-                double want = 20000.0 / std::max(b.tver[j], 1.0);
+                // DB200_WINDOW_NS: the repeat window target (timing experiment; default 20 us)
+                static const double window_ns = std::getenv("DB200_WINDOW_NS") ? std::atof(std::getenv("DB200_WINDOW_NS")) : 20000.0;
+                double want = window_ns / std::max(b.tver[j], 1.0);
                 num = (int)std::min(100.0, std::max(1.0, std::ceil(want)));
             }
             for (int i = 0; i < b.warm[j]; ++i) {
@@ -476,9 +501,11 @@ struct GpuMeasurer : Measurer {
             tuner_status ts = time_windows(b, j, num, b.reps[j], b.tb + j * b.EB, b.number[j]);
             if (ts != TUNER_OK) return ts;
         }
+        const auto hw0 = std::chrono::steady_clock::now();
         tuner_status s = wait_progress(b.prog, b.stall_ms);
         if (s != TUNER_OK) return s;
         cudaError_t se = cudaStreamSynchronize(st);
+        hprof[4] += std::chrono::duration<double>(std::chrono::steady_clock::now() - hw0).count();
         for (auto ge : transient) cudaGraphExecDestroy(ge);
         transient.clear();
         if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize (timing)");
@@ -608,7 +635,9 @@ struct GpuMeasurer : Measurer {
         b.execs.assign(n, nullptr);
         b.stall_ms = std::max(5000.0, 4.0 * t->opts.timeout_ms);
 
+        const auto hp0 = std::chrono::steady_clock::now();
         tuner_status s = n ? phase_verify(pts, b, out) : TUNER_OK;
+        const auto hp1 = std::chrono::steady_clock::now();
         // early cut (SURVEY d.5, R-M3): rank hopeless candidates by their verify run and time
         // clearly non-competitive ones (> 1.5x) with 3 repeats instead of R
         double vmin = INFINITY;
@@ -631,7 +660,12 @@ struct GpuMeasurer : Measurer {
                 }
             }
         }
+        const auto hp2 = std::chrono::steady_clock::now();
         s = n ? phase_time(b, out) : TUNER_OK;
+        const auto hp3 = std::chrono::steady_clock::now();
+        hprof[0] += std::chrono::duration<double>(hp1 - hp0).count();
+        hprof[1] += std::chrono::duration<double>(hp3 - hp2).count();
+        hprof_n += n;
         const bool tier3 = tiers && t->opts.number <= 0;
         double cmin = INFINITY;
         if (s == TUNER_OK)
@@ -642,7 +676,9 @@ struct GpuMeasurer : Measurer {
         const double best = std::min(best_coarse, cmin);
         if (collective) best_coarse = best;
         if (n == 0) return TUNER_OK;
+        const auto hp4 = std::chrono::steady_clock::now();
         s = phase_precise(b, out, best);
+        hprof[2] += std::chrono::duration<double>(std::chrono::steady_clock::now() - hp4).count();
         for (size_t j = 0; j < n; ++j) t->stats.precise += b.precise[j];
         return s;
     }
