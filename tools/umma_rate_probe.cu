@@ -12,13 +12,21 @@
 using namespace db200;
 
 template <int N, int MODE>
-__global__ void probe(int iters, int stages, unsigned long long* out) {
+__global__ void probe(int iters, int stages, unsigned long long* out, int fill) {
     extern __shared__ uint8_t raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar;
     __shared__ uint32_t tslot;
     const int tid = threadIdx.x, warp = tid >> 5;
-    for (int i = tid; i < (8 * 16384) / 16; i += blockDim.x) reinterpret_cast<uint4*>(base)[i] = make_uint4(0, 0, 0, 0);
+    // operands: zeros, or (FILL = 1) pseudo-random bf16 in [-1, 1) -- the tensor pipe's rate may
+    // depend on the data it switches
+    for (int i = tid; i < (8 * 16384) / 4; i += blockDim.x) {
+        uint32_t h = (uint32_t)i * 2654435761u;
+        h ^= h >> 15;
+        h *= 2246822519u;
+        const uint32_t lo = 0x3F80u | (h & 0x807Fu), hi = 0x3F00u | ((h >> 16) & 0x807Fu);
+        reinterpret_cast<uint32_t*>(base)[i] = fill ? (lo | (hi << 16)) : 0u;
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (tid == 0) {
         tc::mbar_init(tc::smem_u32(&bar), 1);
@@ -59,12 +67,12 @@ __global__ void probe(int iters, int stages, unsigned long long* out) {
 }
 
 template <int N, int MODE>
-void run(int iters, unsigned long long* d) {
+void run(int iters, unsigned long long* d, int fill) {
     const int smem = 1024 + 8 * 16384;
     cudaFuncSetAttribute(probe<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     unsigned long long h[2];
     for (int rep = 0; rep < 2; ++rep) {
-        probe<N, MODE><<<1, 128, smem>>>(iters, 4, d);
+        probe<N, MODE><<<1, 128, smem>>>(iters, 4, d, fill);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
             printf("error %s\n", cudaGetErrorString(e));
@@ -72,20 +80,20 @@ void run(int iters, unsigned long long* d) {
         }
     }
     cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-    printf("N=%3d mode %d (%s): issue %.1f cyc/MMA, complete %.1f cyc/MMA (floor 128*N/256 = %d)\n", N, MODE,
-           MODE ? "ring index with runtime divisions" : "constant descriptor step", (double)h[0] / iters,
-           (double)h[1] / iters, 128 * N / 256);
+    printf("N=%3d mode %d (%s), %s operands: issue %.1f cyc/MMA, complete %.1f cyc/MMA (floor 128*N/256 = %d)\n", N,
+           MODE, MODE ? "ring index with runtime divisions" : "constant descriptor step", fill ? "random" : "zero",
+           (double)h[0] / iters, (double)h[1] / iters, 128 * N / 256);
 }
 
 int main() {
     unsigned long long* d;
     cudaMalloc(&d, 16);
     const int iters = 4096;
-    run<64, 0>(iters, d);
-    run<64, 1>(iters, d);
-    run<128, 0>(iters, d);
-    run<128, 1>(iters, d);
-    run<256, 0>(iters, d);
-    run<256, 1>(iters, d);
+    for (int fill = 0; fill < 2; ++fill) {
+        run<64, 0>(iters, d, fill);
+        run<64, 1>(iters, d, fill);
+        run<128, 0>(iters, d, fill);
+        run<256, 0>(iters, d, fill);
+    }
     return 0;
 }
