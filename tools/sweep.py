@@ -32,7 +32,8 @@ def main():
     ap.add_argument("--budget", type=int, default=100)
     ap.add_argument("--baseline", type=int, default=10000)
     ap.add_argument("--max-layers", type=int, default=0, help="per model, 0 = all")
-    ap.add_argument("--early-cut", type=float, default=4.0)
+    ap.add_argument("--early-cut", type=float, default=2.0, help="R-M3 (as bench.py)")
+    ap.add_argument("--repeats", type=int, default=3, help="R-M2: timed windows per candidate (as bench.py)")
     ap.add_argument("--sketch-factor", type=float, default=1.5)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -97,7 +98,7 @@ def main():
                    "shape": {k: v for k, v in L.items() if k not in ("name", "count", "op")}}
             t0 = time.perf_counter()
             tu = Tuner(L["op"], shape, dtype=a.dtype, spaces=spaces, x=xd, w=wd, y=y, seed=0,
-                       early_cut=a.early_cut)
+                       early_cut=a.early_cut, repeats=a.repeats)
             smp = tu.evolve(a.n_sample)
             if not smp:
                 rec["skipped"] = "no statically valid schedule"
@@ -112,7 +113,7 @@ def main():
             rep = min(reps, key=lambda r: r["best_cost"])
             t1 = time.perf_counter()
             bl = Tuner(L["op"], shape, dtype=a.dtype, spaces=spaces, x=xd, w=wd, y=y, seed=7919,
-                       early_cut=a.early_cut)
+                       early_cut=a.early_cut, repeats=a.repeats)
             bl.sample(a.baseline)
             t2 = time.perf_counter()
             bb = bl.best()
