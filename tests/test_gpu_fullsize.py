@@ -43,23 +43,31 @@ def tune_and_check(L, dtype, n_sample, samples=3000, seed=0, sketch=None):
     smp = t.sample(n_sample)
     assert smp and all(s.status == "ok" for s in smp), [s for s in smp if s.status != "ok"][:3]
     rep = t.droplet(t.best().point, 100)
-    y.fill_(float("nan"))
-    t.run(rep["best"], xd, wd, y)
-    torch.cuda.synchronize()
-    yv = y.cpu().numpy().ravel()
+    n_out = int(np.prod(out_shape(L)))
     rng = np.random.Generator(np.random.PCG64(seed))
-    idx = np.unique(np.concatenate([rng.integers(0, yv.size, samples), [0, yv.size - 1]])).astype(np.int64)
+    idx = np.unique(np.concatenate([rng.integers(0, n_out, samples), [0, n_out - 1]])).astype(np.int64)
     if L["op"] == "conv2d":
         yo, ao = oc.conv2d_at(x, w, idx, L["stride"], L["pad"], L["dil"])
     else:
         xb = x if x.ndim == 3 else x[None]
         wb = w if w.ndim == 3 else w[None]
         yo, ao = oc.bmm_at(xb, wb, idx)
-    err = on.max_rel_err(yv[idx], yo, ao)
     tol = on.TOL_F32 if dtype == "f32" else on.TOL_BF16
-    assert err <= tol, (L["name"], t.values(rep["best"]), err)
-    assert np.all(np.isfinite(yv)), "every output written"
-    return t.values(rep["best"]), rep["best_cost"], err
+    # the chosen schedule, then the best point of every other sketch the tuner searched (each a
+    # different kernel family at full size)
+    pts = [rep["best"]] + [sb.point for sb in (t.best_of_sketch(sid) for sid, _ in t.spaces)
+                           if sb is not None and sb.point != rep["best"]]
+    errs = []
+    for p in pts:
+        y.fill_(float("nan"))
+        t.run(p, xd, wd, y)
+        torch.cuda.synchronize()
+        yv = y.cpu().numpy().ravel()
+        err = on.max_rel_err(yv[idx], yo, ao)
+        assert err <= tol, (L["name"], p[0], t.values(p), err)
+        assert np.all(np.isfinite(yv)), ("every output written", p[0], t.values(p))
+        errs.append(err)
+    return t.values(rep["best"]), rep["best_cost"], max(errs), len(pts)
 
 
 @pytest.mark.parametrize("L", [RESNET18[0], RESNET18[1], RESNET50[20], CONFIG1], ids=lambda L: L["name"])
@@ -131,3 +139,9 @@ def test_statistical_droplet_measured_mode():
     for a, c in zip(rep["traj"], rep["traj"][1:]):
         from oracle.stats import wilcoxon_p
         assert wilcoxon_p(t.timings(c), t.timings(a)) < 0.05
+
+
+def test_fullsize_bf16_halo_sketch():
+    # the halo row-tile sketch alone on VGG-16 conv1_2 (b16, 224 x 224: 2 pixel tiles per row, the
+    # second ragged; CTAs run through several rows and images)
+    print(tune_and_check(VGG16[1], "bf16", 60, sketch=11))
