@@ -9,8 +9,12 @@ One *step* = one layer's full tuning job (every §8(a) row): sampler, dispatch,
 execution, verification, timing, sharded all-gather, best-of-N, Droplet, and
 the 10k baseline.  Steps take the layers round-robin (ResNet-18 then ResNet-50).
 value = candidates measured per second over the timed steps (whole job, all
-ranks).  Launch: `python bench.py [--gpus N --steps K --warmup W]`; N > 1 under
-torchrun (one rank per GPU, NCCL).  `--impl reference` times the oracle.
+ranks).  Every candidate is executed and verified; the cost of one is the median
+of R = 3 timed windows (the paper's "averages of three samples"; R-M2),
+near-best ones are re-timed over 200 us windows (R-M4), and ones whose verify run
+is over 2x the best verify run are ranked by that run (R-M3; `early_cut_frac`).
+Launch: `python bench.py [--gpus N --steps K --warmup W]`; N > 1 under torchrun
+(one rank per GPU, NCCL).  `--impl reference` times the oracle.
 """
 from __future__ import annotations
 
