@@ -584,6 +584,8 @@ def main():
         "tuning_wall_s": {"dpansor": round(dp_wall, 3), "baseline_10k": round(bl_wall, 3),
                           "speedup": round(bl_wall / dp_wall, 2) if dp_wall > 0 else None},
         "early_cut_frac": round(n_cut / max(1, cands), 4), "precise_frac": round(n_prec / max(1, cands), 4),
+        # the candidates that got the full timing (R windows, not ranked by their verify run alone)
+        "fully_timed_candidates_per_s": round((cands - n_cut) / (tot_ms / 1e3), 1) if tot_ms > 0 else None,
         "bf16": bf16,
         "per_layer": per,
         "quality_dp_over_10k": {"retimed": "rt_dp_ns" in (tuned[0] if tuned else {}),
