@@ -76,3 +76,20 @@ def test_instantiation_lists_match_their_generator():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gen_instantiations.py"), "--check"],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_sketch_valid_error_paths():
+    """tuner_sketch_valid: ERANGE for an unknown sketch, EDIM for a wrong value count, EINVAL for a bad
+    shape (include/tuner.h); a valid query answers without a device."""
+    import pytest as _pt
+
+    from paper_2406_20037_b200 import TunerError, sketch_space, sketch_valid
+    shape = {"N": 1, "C": 64, "H": 56, "W": 56, "K": 64, "R": 3, "S": 3, "pad": (1, 1)}
+    v = [s[0] for s in sketch_space(1)]
+    assert isinstance(sketch_valid("conv2d", shape, 1, v), bool)
+    with _pt.raises(TunerError):
+        sketch_valid("conv2d", shape, 99, v)          # ERANGE
+    with _pt.raises(TunerError):
+        sketch_valid("conv2d", shape, 1, v[:-1])      # EDIM
+    with _pt.raises(TunerError):
+        sketch_valid("conv2d", dict(shape, C=0), 1, v)  # EINVAL
