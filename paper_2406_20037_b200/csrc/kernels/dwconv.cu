@@ -103,6 +103,10 @@ __global__ void __launch_bounds__(512) dwconv_kernel(const DwParams p) {
     const int RS = p.R * p.S;
     const TIn* __restrict__ X = (const TIn*)p.x;
     const TIn* __restrict__ Wt = (const TIn*)p.w;
+    // programmatic dependent launch: the next kernel may launch now; this one reads only after its
+    // predecessor completed
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    griddep_wait();
 
     // filters of this CTA's channels, transposed to [rs][channel] (zero past C)
     float* ws = sm;
@@ -187,7 +191,9 @@ __global__ void __launch_bounds__(512) dwconv_win_kernel(const DwParams p) {
     const int q0 = (blockIdx.y * blockDim.y + threadIdx.y) * TQ;
     const int n = blockIdx.z / p.tiles_p;
     const int p0 = ((blockIdx.z % p.tiles_p) * blockDim.z + threadIdx.z) * TP;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // PDL, as dwconv_kernel
     if (c >= p.C || q0 >= p.Q || p0 >= p.P) return;
+    griddep_wait();
     const TIn* __restrict__ X = (const TIn*)p.x + (long long)n * p.H * p.W * p.C + c;
     const TIn* __restrict__ Wt = (const TIn*)p.w + (long long)c * KS * KS;
 
@@ -268,9 +274,17 @@ cudaError_t dwconv_win_launch(const LaunchCtx& c) {
     p.ih = p.iw = 0;
     dim3 grid((unsigned)((p.C + ct * VEC - 1) / (ct * VEC)), (unsigned)((p.Q + qt * TQ - 1) / (qt * TQ)),
               (unsigned)(p.N * p.tiles_p));
-    dwconv_win_kernel<TIn, VEC, TQ, TP, KS, SH><<<grid, dim3(ct, qt, pt), 0, c.stream>>>(p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(ct, qt, pt);
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    pdl_attr(attr[0]);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, dwconv_win_kernel<TIn, VEC, TQ, TP, KS, SH>, p);
     count_launches(1);
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <typename TIn, int VEC, int TQ, bool SMEM>
@@ -296,9 +310,18 @@ cudaError_t dwconv_launch(const LaunchCtx& c) {
     const size_t smem = dwconv_smem_bytes(p.R * p.S, ct * VEC, SMEM ? p.ih * p.iw : 0);
     dim3 grid((unsigned)((p.C + ct * VEC - 1) / (ct * VEC)), (unsigned)((p.Q + qt * TQ - 1) / (qt * TQ)),
               (unsigned)(p.N * p.tiles_p));
-    kern<<<grid, dim3(ct, qt, pt), smem, c.stream>>>(p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(ct, qt, pt);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    pdl_attr(attr[0]);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
     count_launches(1);
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // registry key: (VEC, TQ, ALG, TP, KS * 4 + SH) for ALG 0; (VEC, TQ, ALG, 1, 0) for ALG 1 / 2
